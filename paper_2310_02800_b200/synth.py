@@ -1,0 +1,166 @@
+"""Seeded synthetic temporal graphs — the ONLY module shared by the oracle
+side (tests/, bench.py's cpu_baseline) and the CUDA side.  It holds none of
+the method's arithmetic: it only draws edges.
+
+Shapes follow the paper's datasets (Table 3) as planned
+in SURVEY.md §8(d) "Synthetic generator":
+
+1. vertex activity ``w_i = (π(i)+1)^-α`` with π a seeded permutation, shares
+   capped at ``cap`` (hubs both send and receive);
+2. ``S ≈ m/μ`` *sessions* (μ = temporal/static edge ratio of the dataset):
+   a pair (u~w, v~w, u≠v except a 0.1 % self-loop rate), a start
+   ``s ~ U[0, span)``, ``Geom(1/μ)`` events (mean μ) at ``s + Σ Exp(β)``
+   (integer seconds), each event reversed (v→u) with probability ``p_reply``;
+3. email shape only: with probability ``fanout`` an event is copied to 1-4
+   extra recipients at the **same timestamp** (exercises the tie rule Q1);
+4. clip to the span, keep exactly ``m`` events in session order, order by
+   ``(t, session, event)``.
+
+All randomness comes from ``numpy.random.default_rng(seed)`` (PCG64), so a
+config + seed fixes the graph bit for bit.  Seeds: ``231002800 + config``.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+DAY = 86400
+YEAR = 365 * DAY
+SEED_BASE = 231002800
+
+
+@dataclasses.dataclass(frozen=True)
+class GraphSpec:
+    name: str
+    n: int
+    m: int
+    span: int          # seconds
+    mu: float          # mean events per session (temporal/static edge ratio)
+    alpha: float       # power-law exponent of vertex activity
+    cap: float         # max activity share of one vertex
+    beta: float        # mean inter-event gap inside a session (s)
+    fanout: float = 0.0
+    p_reply: float = 0.3
+    p_self: float = 0.001
+    t0: int = 1_200_000_000   # epoch-like base time
+
+
+# SURVEY.md §8(d) table (α, cap, β, p_reply are proposals, not paper values)
+SPECS = {
+    "C1": GraphSpec("C1 tiny", 1000, 20_000, 7 * DAY, 2.0, 1.0, 0.03, 3600.0),
+    "C2": GraphSpec("C2 email-Eu-core-shaped", 986, 332_334, 803 * DAY, 13.3, 1.0, 0.03, 600.0, fanout=0.1),
+    "C3": GraphSpec("C3 wiki-talk-shaped", 1_140_149, 7_833_140, int(6.24 * YEAR), 2.81, 1.0, 0.01, 3600.0),
+    "C4": GraphSpec("C4 stackoverflow-shaped", 2_601_977, 63_497_050, int(7.6 * YEAR), 1.82, 0.8, 0.003, 3600.0),
+}
+
+
+def activity(n: int, alpha: float, cap: float, rng: np.random.Generator) -> np.ndarray:
+    """Vertex sampling probabilities: (π(i)+1)^-α, shares clipped at ``cap``."""
+    rank = rng.permutation(n).astype(np.float64)
+    p = (rank + 1.0) ** (-alpha)
+    p /= p.sum()
+    if cap * n < 1.0:
+        cap = 1.0 / n
+    for _ in range(100):
+        over = p > cap
+        if not over.any():
+            break
+        excess = float((p[over] - cap).sum())
+        p[over] = cap
+        free = p < cap
+        p[free] += excess * p[free] / p[free].sum()
+    return p / p.sum()
+
+
+def generate(spec: GraphSpec, seed: int, *, m: int | None = None, shuffle: bool = False):
+    """Returns (src u32[m], dst u32[m], t i64[m], n).  Sorted by time unless
+    ``shuffle`` (a seeded permutation of the input order)."""
+    rng = np.random.default_rng(seed)
+    n = spec.n
+    m = spec.m if m is None else m
+    p = activity(n, spec.alpha, spec.cap, rng)
+    cdf = np.cumsum(p)
+    cdf[-1] = 1.0
+
+    def draw(k):
+        return np.minimum(np.searchsorted(cdf, rng.random(k), side="right"), n - 1).astype(np.int64)
+
+    per_session = spec.mu * (1.0 + spec.fanout * 2.5)
+    S = int(math.ceil(m / per_session * 1.15)) + 64
+    u = draw(S)
+    v = draw(S)
+    for _ in range(16):
+        bad = np.nonzero(u == v)[0]
+        if bad.size == 0:
+            break
+        v[bad] = draw(bad.size)
+    bad = u == v
+    v[bad] = (u[bad] + 1) % n
+    selfl = rng.random(S) < spec.p_self
+    v[selfl] = u[selfl]
+    start = rng.integers(0, spec.span, S, dtype=np.int64)
+    k = rng.geometric(1.0 / spec.mu, S).astype(np.int64)
+
+    total = int(k.sum())
+    sess = np.repeat(np.arange(S, dtype=np.int64), k)
+    first = np.zeros(total, bool)
+    first[np.cumsum(k) - k] = True
+    gap = rng.exponential(spec.beta, total)
+    gap[first] = 0.0
+    cg = np.cumsum(gap)
+    base = cg[np.cumsum(k) - k]
+    off = np.floor(cg - np.repeat(base, k)).astype(np.int64)
+    t = start[sess] + off
+    es = u[sess].copy()
+    ed = v[sess].copy()
+    rev = rng.random(total) < spec.p_reply
+    es[rev], ed[rev] = ed[rev], es[rev].copy()
+
+    if spec.fanout > 0:
+        fo = rng.random(total) < spec.fanout
+        idx = np.nonzero(fo)[0]
+        extra = rng.integers(1, 5, idx.size)
+        rep = np.repeat(idx, extra)
+        xs = es[rep]
+        xd = draw(rep.size)
+        clash = xd == xs
+        xd[clash] = (xs[clash] + 1) % n
+        # interleave: each extra copy follows its parent event
+        order_key = np.concatenate([np.arange(total, dtype=np.int64) * 8,
+                                    rep * 8 + 1 + (np.arange(rep.size) - np.repeat(np.cumsum(extra) - extra, extra))])
+        es = np.concatenate([es, xs]); ed = np.concatenate([ed, xd]); t = np.concatenate([t, t[rep]])
+        o = np.argsort(order_key, kind="stable")
+        es, ed, t = es[o], ed[o], t[o]
+
+    keep = t < spec.span
+    es, ed, t = es[keep], ed[keep], t[keep]
+    if es.size < m:
+        raise RuntimeError(f"generator produced {es.size} < {m} events; raise oversampling")
+    es, ed, t = es[:m], ed[:m], t[:m]
+    o = np.argsort(t, kind="stable")            # (t, session, event)
+    src = es[o].astype(np.uint32)
+    dst = ed[o].astype(np.uint32)
+    tt = (t[o] + spec.t0).astype(np.int64)
+    if shuffle:
+        prm = np.random.default_rng(seed ^ 0x5EED).permutation(m)
+        src, dst, tt = src[prm], dst[prm], tt[prm]
+    return src, dst, tt, n
+
+
+def config_graph(name: str, *, m: int | None = None, shuffle: bool = False, seed_offset: int = 0):
+    idx = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}[name]
+    return generate(SPECS[name], SEED_BASE + idx + seed_offset, m=m, shuffle=shuffle)
+
+
+def tiny_graph(seed: int, n: int = 8, m: int = 40, tmax: int = 30, p_self: float = 0.05):
+    """Small random multigraph for brute-force checks: many duplicate
+    timestamps, parallel edges and some self-loops; input order random."""
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    s = rng.random(m) < p_self
+    dst[s] = src[s]
+    t = rng.integers(0, tmax + 1, m).astype(np.int64)
+    return src, dst, t, n

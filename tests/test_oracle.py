@@ -1,0 +1,277 @@
+"""Pins for the oracle (oracle/tmoracle.c, Algorithm 1) against things other
+than itself: the paper's worked rules, the literal definition (brute force),
+closed forms, a library routine (networkx monomorphisms) at δ = ∞, and
+symmetries/invariants of the definition."""
+from __future__ import annotations
+
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from brute import brute, prefix_count, sorted_edges, verify_match
+from cases import CATALOG, INF, random_fine, random_motif, reverse_prefix_connected
+from golden_io import all_fixtures
+from paper_2310_02800_b200 import motifs as M
+from paper_2310_02800_b200 import synth
+from pins import census36_sum, static_time_ordered_count, time_reverse, two_node_closed_form
+
+
+def ocount(src, dst, t, n, motif, delta, fine=None):
+    return oracle.Graph(src, dst, t, n).mine(motif, delta, fine)["count"]
+
+
+def orows(src, dst, t, n, motif, delta, fine=None):
+    r = oracle.Graph(src, dst, t, n).mine(motif, delta, fine, enumerate_=True)
+    return sorted(tuple(int(x) for x in row) for row in r["rows"]), r["n_total"]
+
+
+# --------------------------------------------------------------- worked examples
+@pytest.mark.parametrize("fx", all_fixtures(), ids=lambda f: f["name"])
+def test_golden(fx):
+    rows, n_total = orows(fx["src"], fx["dst"], fx["t"], fx["n"], fx["motif"], fx["delta"], fx["fine"])
+    assert n_total == fx["count"]
+    assert rows == fx["rows"]
+    # the fixture itself is consistent with the literal definition
+    assert brute(fx["src"], fx["dst"], fx["t"], fx["motif"], fx["delta"], fx["fine"]) == fx["rows"]
+
+
+# ------------------------------------------------------------------ brute force
+def _trials(n_trials, seed0, L_choices, m_range, tmax=30):
+    rng = random.Random(seed0)
+    for k in range(n_trials):
+        L = rng.choice(L_choices)
+        motif = rng.choice([c for c in CATALOG if len(c) == L] + [random_motif(rng, L)])
+        m = rng.randint(*m_range)
+        n = rng.randint(3, 9)
+        src, dst, t, n = synth.tiny_graph(seed0 * 1000 + k, n=n, m=m, tmax=tmax)
+        delta = rng.choice([0, 3, 10, 25, INF])
+        fine = random_fine(rng, L)
+        yield src, dst, t, n, motif, delta, fine
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_oracle_vs_brute_L123(seed):
+    for src, dst, t, n, motif, delta, fine in _trials(40, 100 + seed, [1, 2, 3], (0, 70)):
+        rows, n_total = orows(src, dst, t, n, motif, delta, fine)
+        b = brute(src, dst, t, motif, delta, fine)
+        assert rows == b, (motif, delta, fine)
+        assert n_total == len(b) == ocount(src, dst, t, n, motif, delta, fine)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_oracle_vs_brute_L45(seed):
+    for src, dst, t, n, motif, delta, fine in _trials(20, 200 + seed, [4, 5], (5, 36), tmax=40):
+        if delta == INF and len(motif) == 5:
+            delta = 25
+        rows, n_total = orows(src, dst, t, n, motif, delta, fine)
+        assert rows == brute(src, dst, t, motif, delta, fine), (motif, delta, fine)
+
+
+def test_search_nodes_equal_prefix_counts():
+    """nodes[l] (partial matches with l edges whose next window is searched) is
+    the count of the l-edge prefix motif; every window is searched once."""
+    for src, dst, t, n, motif, delta, fine in _trials(30, 7, [2, 3, 4], (5, 40)):
+        st = oracle.Graph(src, dst, t, n).mine(motif, delta, fine)["stats"]
+        pc = prefix_count(src, dst, t, motif, delta, fine)
+        assert st["nodes"][1:len(motif)] == pc[:-1]
+        assert st["matches"] == pc[-1]
+
+
+def test_window_sum_single_list_motifs():
+    """Σ|window| for motifs whose every level has one bound endpoint (no list
+    choice): windows are the bound vertex's out/in edges after e_l within δ
+    and δ_l, counted here from brute-force prefix matches."""
+    rng = random.Random(11)
+    for k in range(30):
+        motif = rng.choice([M.P3, M.STAR3, M.PATH2, [(0, 1), (2, 1), (3, 2)]])
+        src, dst, t, n = synth.tiny_graph(500 + k, n=6, m=rng.randint(5, 45), tmax=30)
+        delta = rng.choice([0, 5, 12, INF])
+        fine = random_fine(rng, len(motif))
+        S, D, T, _ = sorted_edges(src, dst, t)
+        exp = 0
+        for l in range(1, len(motif)):
+            fl = None if fine is None else fine[:l - 1]
+            for tup in brute(src, dst, t, motif[:l], delta, fl):
+                phi = {}
+                for (a, b), e in zip(motif[:l], tup):
+                    phi[a], phi[b] = S[e], D[e]
+                u, v = motif[l]
+                f = INF if fine is None or fine[l - 1] is None else fine[l - 1]
+                for c in range(tup[-1] + 1, len(S)):
+                    ok_list = (S[c] == phi[u]) if u in phi else (D[c] == phi[v])
+                    if ok_list and T[c] - T[tup[0]] <= delta and T[c] - T[tup[-1]] <= f:
+                        exp += 1
+        st = oracle.Graph(src, dst, t, n).mine(motif, delta, fine)["stats"]
+        assert st["window_sum"] == exp
+
+
+# ----------------------------------------------------------------- closed forms
+def test_delta_inf_equals_static_time_ordered_count():
+    rng = random.Random(5)
+    for k in range(40):
+        L = rng.choice([2, 3, 4])
+        motif = rng.choice([c for c in CATALOG if len(c) == L] + [random_motif(rng, L, max_v=4)])
+        src, dst, t, n = synth.tiny_graph(900 + k, n=rng.randint(3, 7), m=rng.randint(4, 30), tmax=12)
+        assert ocount(src, dst, t, n, motif, INF) == static_time_ordered_count(src, dst, t, motif), motif
+
+
+def test_two_node_closed_form():
+    for k in range(30):
+        src, dst, t, n = synth.tiny_graph(1300 + k, n=4, m=60, tmax=40)
+        for delta in (0, 4, 13, INF):
+            s = sum(ocount(src, dst, t, n, mm, delta) for mm in M.TWO_NODE)
+            assert s == two_node_closed_form(src, dst, t, delta)
+
+
+def test_census36_sum():
+    for k in range(12):
+        src, dst, t, n = synth.tiny_graph(1700 + k, n=5, m=50, tmax=40)
+        for delta in (0, 6, 20):
+            s = sum(ocount(src, dst, t, n, mm, delta) for mm in M.P36)
+            assert s == census36_sum(src, dst, t, delta)
+
+
+def test_single_edge_motif_counts_non_self_loops():
+    src, dst, t, n = synth.tiny_graph(3, n=5, m=200, tmax=50, p_self=0.2)
+    assert ocount(src, dst, t, n, [(0, 1)], 0) == int(np.sum(src != dst))
+
+
+# ---------------------------------------------------------- symmetries/invariants
+def test_delta_monotone_and_fine_subsumption():
+    rng = random.Random(9)
+    for k in range(15):
+        motif = rng.choice(CATALOG[:6])
+        src, dst, t, n = synth.tiny_graph(2000 + k, n=6, m=60, tmax=50)
+        g = oracle.Graph(src, dst, t, n)
+        prev = -1
+        for d in (0, 1, 3, 7, 15, 30, 60, INF):
+            c = g.mine(motif, d)["count"]
+            assert c >= prev
+            prev = c
+            L = len(motif)
+            # every δ_i >= δ: equal to the coarse-only count
+            assert g.mine(motif, d, [d] * (L - 1))["count"] == c
+            # lowering one δ_i never increases the count
+            f = [INF] * (L - 1)
+            f[rng.randrange(L - 1)] = 2
+            assert g.mine(motif, d, f)["count"] <= c
+
+
+def test_time_reversal_direction_reversal_shift_relabel():
+    rng = random.Random(13)
+    for k in range(30):
+        motif = rng.choice([c for c in CATALOG if len(c) >= 2 and reverse_prefix_connected(c)])
+        L = len(motif)
+        src, dst, t, n = synth.tiny_graph(2500 + k, n=6, m=50, tmax=40)
+        delta = rng.choice([3, 10, 25, INF])
+        fine = random_fine(rng, L)
+        base = ocount(src, dst, t, n, motif, delta, fine)
+        rs, rd, rt, rm, rf = time_reverse(src, dst, t, motif, fine)
+        assert ocount(rs, rd, rt, n, rm, delta, rf) == base
+        assert ocount(dst, src, t, n, [(b, a) for a, b in motif], delta, fine) == base
+        assert ocount(src, dst, np.asarray(t) + 10**12, n, motif, delta, fine) == base
+        perm = np.random.default_rng(k).permutation(n).astype(np.uint32)
+        assert ocount(perm[src], perm[dst], t, n, motif, delta, fine) == base
+        sh = np.random.default_rng(k + 1).permutation(len(src))
+        assert ocount(src[sh], dst[sh], t[sh], n, motif, delta, fine) == base or \
+            _ties_reordered(t, sh)
+
+
+def _ties_reordered(t, sh):
+    # shuffling input changes the (t, input index) tie order among equal
+    # timestamps, which can legitimately change counts (reading Q1); only
+    # accept a difference when equal timestamps exist.
+    return len(set(t.tolist())) < len(t)
+
+
+def test_input_order_independence_unique_times():
+    rng = np.random.default_rng(1)
+    for k in range(10):
+        m = 60
+        src, dst, _, n = synth.tiny_graph(3000 + k, n=6, m=m)
+        t = rng.permutation(200)[:m].astype(np.int64)  # unique timestamps
+        base = ocount(src, dst, t, n, M.TRI, 40)
+        sh = rng.permutation(m)
+        assert ocount(src[sh], dst[sh], t[sh], n, M.TRI, 40) == base
+
+
+def test_concatenation_sums():
+    a = synth.tiny_graph(41, n=6, m=50, tmax=30)
+    b = synth.tiny_graph(42, n=6, m=50, tmax=30)
+    for motif in (M.TRI, M.C4, M.PATH2):
+        ca = ocount(*a, motif, 10)
+        cb = ocount(*b, motif, 10)
+        src = np.concatenate([a[0], b[0]]); dst = np.concatenate([a[1], b[1]])
+        t = np.concatenate([a[2], b[2] + 1000])
+        assert ocount(src, dst, t, 6, motif, 10) == ca + cb
+
+
+def test_partition_halo_sums():
+    """A match belongs to the partition holding e_1 (reading Q16); mining each
+    root range [lo,hi) on the edge slice [lo, H_δ(hi-1)] sums to the total
+    (P:1025-1037)."""
+    rng = random.Random(17)
+    for k in range(20):
+        motif = rng.choice(CATALOG)
+        src, dst, t, n = synth.tiny_graph(3500 + k, n=7, m=80, tmax=60)
+        delta = rng.choice([0, 5, 15])
+        S, D, T, _ = sorted_edges(src, dst, t)
+        S, D, T = np.array(S, np.uint32), np.array(D, np.uint32), np.array(T, np.int64)
+        total = ocount(S, D, T, n, motif, delta)
+        cuts = sorted(rng.sample(range(1, 80), 3))
+        bounds = [0] + cuts + [80]
+        s = 0
+        for lo, hi in zip(bounds[:-1], bounds[1:]):
+            ehi = int(np.searchsorted(T, T[hi - 1] + delta, side="right"))  # one past H_δ(hi-1)
+            g = oracle.Graph(S[lo:ehi], D[lo:ehi], T[lo:ehi], n)
+            s += g.mine(motif, delta, root_range=(0, hi - lo))["count"]
+        assert s == total
+
+
+def test_per_root_and_enumeration_consistency():
+    src, dst, t, n = synth.tiny_graph(77, n=6, m=120, tmax=60)
+    g = oracle.Graph(src, dst, t, n)
+    for motif in (M.TRI, M.TT, M.C4):
+        r = g.mine(motif, 20, per_root=True)
+        e = g.mine(motif, 20, enumerate_=True)
+        assert int(r["per_root"].sum()) == r["count"] == e["n_total"]
+        S, D, T, _ = sorted_edges(src, dst, t)
+        rows = [tuple(int(x) for x in row) for row in e["rows"]]
+        assert len(set(rows)) == len(rows)
+        assert all(verify_match(S, D, T, motif, 20, None, row) for row in rows)
+        roots = np.bincount([row[0] for row in rows], minlength=len(S))
+        assert np.array_equal(roots, r["per_root"].astype(np.int64))
+
+
+def test_truncated_enumeration_keeps_exact_total():
+    src, dst, t, n = synth.tiny_graph(78, n=5, m=100, tmax=40)
+    g = oracle.Graph(src, dst, t, n)
+    full = g.mine(M.TRI, 20)["count"]
+    assert full > 5
+    e = g.mine(M.TRI, 20, enumerate_=True, cap=5)
+    assert e["n_total"] == full and len(e["rows"]) == 5
+
+
+def test_multithreaded_equals_single():
+    src, dst, t, n = synth.config_graph("C1")
+    g = oracle.Graph(src, dst, t, n)
+    a = g.mine(M.TRI, 3600, threads=1)
+    b = g.mine(M.TRI, 3600, threads=4)
+    assert a["count"] == b["count"] and a["stats"] == b["stats"]
+
+
+def test_validation():
+    g = oracle.Graph(np.array([0], np.uint32), np.array([1], np.uint32), np.array([0], np.int64), 2)
+    with pytest.raises(oracle.OracleError) as ei:
+        g.mine([(0, 1), (2, 3)], 5)          # prefix-disconnected (Q9)
+    assert ei.value.code == oracle.EUNSUPPORTED
+    with pytest.raises(oracle.OracleError):
+        g.mine([(0, 0)], 5)                  # motif self-loop
+    with pytest.raises(oracle.OracleError):
+        g.mine([(0, 1)], -1)                 # δ < 0
+    with pytest.raises(oracle.OracleError):
+        oracle.Graph(np.array([0], np.uint32), np.array([5], np.uint32), np.array([0], np.int64), 2)
+    e = oracle.Graph(np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.int64), 3)
+    assert e.mine(M.TRI, 10)["count"] == 0   # empty graph is valid
