@@ -1,0 +1,209 @@
+/*
+ * tmotif.h — C ABI of libtmotif.so, a B200-native (sm_100a) δ-temporal motif
+ * miner for the hot path of arxiv 2310.02800 ("Everest").  PAPER.md is cited
+ * as P:<line>.
+ *
+ * The problem: a temporal graph is a set of directed timestamped
+ * edges (u_i, v_i, t_i); a δ-temporal motif is an ordered list of motif edges
+ * (u_i, v_i) (list order = temporal order) plus a window δ and optional
+ * per-gap bounds δ_i.  A match is a tuple of graph edges
+ * (e_1, ..., e_L) with
+ *     e_1 < e_2 < ... < e_L  in the (t, input position) order,
+ *     t(e_L) - t(e_1) <= δ,         t(e_{i+1}) - t(e_i) <= δ_i,
+ * and an injective map φ of motif vertices to graph vertices with
+ * φ(u_i) = src(e_i), φ(v_i) = dst(e_i).  The library counts the
+ * matches or enumerates them into a caller buffer ("enumerated or
+ * counted").  DESIGN.md lists every reading of the paper this encodes
+ * (ties Q1, inclusive bounds Q2, self-loops Q4, unsupported motifs Q9 ...).
+ *
+ * Conventions
+ *  - Every call returns tm_status; TM_OK = 0.  No C++ exception crosses the
+ *    ABI.  On failure tm_last_error() returns a thread-local message.
+ *  - Edge ids: the graph orders its edges stably by (t, input position); the
+ *    id of an edge is its rank in that order (reading Q1).  Enumerated rows
+ *    hold these ids; tm_graph_sorted_to_input maps them back.
+ *  - Timestamps and δ are int64 in the caller's unit.  TM_DELTA_INF = no
+ *    bound.
+ *  - Handles are immutable after creation: concurrent tm_count calls on
+ *    different streams are allowed.  All device work of a call is ordered on
+ *    opts->stream and the call returns after that stream reaches the end of
+ *    the call's work (synchronous).
+ *  - "device pointer" means memory the CUDA device of the handle can address
+ *    (cudaMalloc'ed, e.g. a torch CUDA tensor's data_ptr()).
+ */
+#ifndef TMOTIF_H
+#define TMOTIF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TM_OK = 0,
+    TM_EINVAL = 1,        /* invalid argument (message says which)                  */
+    TM_ENOMEM = 2,        /* device or host allocation failed                       */
+    TM_ECUDA = 3,         /* a CUDA runtime error (message carries cudaGetErrorString) */
+    TM_EUNSUPPORTED = 4,  /* motif outside the supported set (prefix-disconnected, Q9) */
+    TM_TRUNCATED = 5      /* tm_enumerate: more matches than buffer rows            */
+} tm_status;
+
+#define TM_DELTA_INF INT64_MAX
+#define TM_MAX_EDGES 6      /* motif edges L <= 6 (configs use <= 5)                 */
+#define TM_MAX_VERTICES 7   /* distinct motif vertices                               */
+#define TM_MAX_M 2147483647u  /* graph edges m <= 2^31 - 1 (u32 record positions)   */
+
+typedef struct tm_graph tm_graph;
+typedef struct tm_motif tm_motif;
+
+/* ------------------------------------------------------------------ graph */
+
+typedef struct {
+    int device;           /* CUDA device ordinal; -1 = the calling thread's current */
+    void *stream;         /* cudaStream_t for the build; NULL = legacy default      */
+    int input_on_device;  /* 1: src/dst/t are device pointers; 0: host pointers     */
+} tm_graph_opts;
+
+/* Load a temporal graph G = {(src[i], dst[i], t[i])}, i < m and
+ * build, on the device, the chronologically sorted temporal edge list and the
+ * two time-sorted CSR adjacency structures of P:230-231 (out- and
+ * in-adjacency, each record a 64-bit (edge id << 32 | neighbour)).
+ *   src, dst : m vertex ids, each < n_vertices (dense ids; the caller densifies)
+ *   t        : m timestamps, each >= 0; any order (stable sort by (t, i))
+ *   m        : 0 <= m <= TM_MAX_M; m == 0 is a valid empty graph
+ *   o        : may be NULL (device -1, default stream, host input)
+ * Ownership: the inputs are copied; the caller keeps them.  The library owns
+ * *out and its device memory until tm_graph_destroy.  Self-loop edges are
+ * kept (they take edge ids) but can never be matched (injectivity, Q4).
+ * Errors: TM_EINVAL (null pointer with m > 0, id >= n_vertices, t < 0,
+ * m > TM_MAX_M), TM_ENOMEM, TM_ECUDA. */
+tm_status tm_graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m,
+                          uint32_t n_vertices, const tm_graph_opts *o, tm_graph **out);
+
+tm_status tm_graph_destroy(tm_graph *g);
+
+/* m, n_vertices and device ordinal of a graph (any pointer may be NULL). */
+tm_status tm_graph_info(const tm_graph *g, uint64_t *m, uint32_t *n_vertices, int *device);
+
+/* perm[id] = input position of edge id, for id < m.  perm: host, m entries,
+ * caller-owned. */
+tm_status tm_graph_sorted_to_input(const tm_graph *g, uint64_t *perm);
+
+/* Copy the sorted edge list (host buffers of m entries each; any may be NULL). */
+tm_status tm_graph_sorted_edges(const tm_graph *g, uint32_t *src, uint32_t *dst, int64_t *t);
+
+/* ------------------------------------------------------------------ motif */
+
+/* Define a δ-temporal motif with optional fine-grained bounds.
+ *   L        : number of motif edges, 1..TM_MAX_EDGES
+ *   mu, mv   : L motif edges (mu[i] -> mv[i]); list order = temporal order.
+ *              Any vertex labels < 64; they are relabelled by first appearance.
+ *   delta    : δ >= 0, or TM_DELTA_INF
+ *   fine     : NULL, or L-1 entries: fine[i] = δ_{i+1} bounds t(e_{i+2}) -
+ *              t(e_{i+1}) (0-based gaps), each >= 0 or TM_DELTA_INF
+ * Ownership: inputs copied; library owns *out until tm_motif_destroy.
+ * Errors: TM_EINVAL (L out of range, mu[i] == mv[i] (motif self-loop),
+ * label >= 64, more than TM_MAX_VERTICES vertices, δ < 0, δ_i < 0);
+ * TM_EUNSUPPORTED when an edge after the first touches no earlier motif
+ * vertex (Algorithm 1's all-edges candidate list; reading Q9). */
+tm_status tm_motif_create(uint32_t L, const uint32_t *mu, const uint32_t *mv, int64_t delta,
+                          const int64_t *fine, tm_motif **out);
+
+tm_status tm_motif_destroy(tm_motif *mo);
+
+/* Whether the motif runs on a compile-time specialised kernel (1) or on the
+ * generic kernel with a runtime plan (0). */
+tm_status tm_motif_specialised(const tm_motif *mo, int *specialised);
+
+/* ------------------------------------------------------------------- runs */
+
+typedef struct {
+    void *stream;            /* cudaStream_t; NULL = legacy default stream           */
+    uint64_t root_lo;        /* mine the search trees rooted at edge ids           */
+    uint64_t root_hi;        /*   [root_lo, min(root_hi, m)); default 0, UINT64_MAX  */
+    uint64_t edge_id_offset; /* added to every enumerated id (partitions, §8(e))     */
+    int canonical;           /* tm_enumerate: sort rows lexicographically           */
+    int buffers_on_device;   /* output buffers are device pointers                   */
+    uint32_t grid_ctas;      /* 0 = auto (persistent: SMs x resident CTAs)           */
+    uint32_t block_threads;  /* 0 = auto                                              */
+} tm_run_opts;
+
+/* Fill *o with the defaults above. */
+void tm_run_opts_default(tm_run_opts *o);
+
+/* Exact number of matches whose first edge e_1 lies in the root range (a
+ * match belongs to its root edge, reading Q16).  *count: host. */
+tm_status tm_count(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o, uint64_t *count);
+
+/* Enumerate the matches of the root range into buf: row r occupies
+ * buf[r*L .. r*L+L) (u32 edge ids + o->edge_id_offset).  buf is caller-owned,
+ * cap rows (host, or device when o->buffers_on_device).  Row order is
+ * unspecified unless o->canonical.  *n_total (host) always receives the exact
+ * match count; *n_written (host) = min(n_total, cap).  Returns TM_TRUNCATED
+ * (rows beyond cap dropped, which subset is unspecified) when n_total > cap
+ * ("the user must define the number of matches to be enumerated"). */
+tm_status tm_enumerate(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o, uint32_t *buf,
+                       uint64_t cap, uint64_t *n_total, uint64_t *n_written);
+
+/* Per-root counts: counts[i] = number of matches with e_1 = roots[i].
+ * roots (n ids < m) and counts (n entries) are host pointers, or device
+ * pointers when o->buffers_on_device.  Root range fields of o are ignored. */
+tm_status tm_count_roots(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o,
+                         const uint64_t *roots, uint64_t n, uint64_t *counts);
+
+/* Search-tree instrumentation of one tm_count-equivalent run (debug kernel,
+ * not the timed path).  nodes[l] (l = 1..L-1): partial matches with l edges
+ * whose candidate window for motif edge l+1 was searched (each exactly once,
+ * the P:719-723 candidate-caching invariant); window_sum: Σ window sizes;
+ * list_sum: Σ lengths of the adjacency lists searched; probe_sum: Σ
+ * ceil(log2(len+1)); matches. */
+typedef struct {
+    uint64_t nodes[8];
+    uint64_t window_sum;
+    uint64_t list_sum;
+    uint64_t probe_sum;
+    uint64_t matches;
+} tm_search_stats;
+
+tm_status tm_search_stats_run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o,
+                              tm_search_stats *out);
+
+/* Device times (ms, CUDA events on o->stream) of the calling thread's last
+ * tm_count / tm_enumerate / tm_count_roots: horizon construction, the mining
+ * kernel, and the whole call.  launches: kernels this library launched in it. */
+typedef struct {
+    float horizon_ms;
+    float mine_ms;
+    float total_ms;
+    uint32_t launches;
+    uint32_t grid_ctas;
+    uint32_t block_threads;
+} tm_run_info;
+
+tm_status tm_last_run_info(tm_run_info *out);
+
+/* ------------------------------------------------------------ partitioning */
+
+/* Multi-GPU time-range partition plan.
+ * Splits roots [0, m) of a sorted edge list into P contiguous ranges
+ * [root_lo[p], root_lo[p+1]) (root_lo has P+1 entries, root_lo[0]=0,
+ * root_lo[P]=m) balanced by `weights` (per-root work proxy; NULL = the
+ * δ-window length H_δ(r) - r), and returns edge_hi[p] = one past the last
+ * edge rank p must hold: H_δ(root_lo[p+1]-1) + 1 (its forward δ-halo).
+ * t_sorted: host, m timestamps in edge-id order.  delta: the motif's
+ * effective reach min(δ, Σδ_i).  Errors: TM_EINVAL. */
+tm_status tm_partition_plan(const int64_t *t_sorted, uint64_t m, int64_t delta, uint32_t P,
+                            const uint64_t *weights, uint64_t *root_lo, uint64_t *edge_hi);
+
+/* Thread-local message of the last non-OK status ("" if none). */
+const char *tm_last_error(void);
+
+/* Library version string. */
+const char *tm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TMOTIF_H */

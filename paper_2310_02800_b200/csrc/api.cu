@@ -1,0 +1,483 @@
+// C ABI of libtmotif (include/tmotif.h): argument validation, motif
+// canonicalisation, the per-query horizon construction and the mining
+// launch.  Every step of the hot path runs in this library's kernels.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+#include "catalog.cuh"
+
+namespace tmg {
+
+tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m, uint32_t n,
+                       const tm_graph_opts *o, tm_graph **out);
+void graph_destroy(tm_graph *g);
+cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, cudaStream_t s);
+
+namespace {
+thread_local std::string g_err;
+thread_local tm_run_info g_info = {};
+
+std::vector<CatalogEntry> &catalog() {
+    static std::vector<CatalogEntry> v = [] {
+        std::vector<CatalogEntry> c;
+        register_named(c);
+        register_p36_part<0>(c);
+        register_p36_part<1>(c);
+        register_p36_part<2>(c);
+        register_p36_part<3>(c);
+        return c;
+    }();
+    return v;
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+std::mutex g_attr_mu;
+std::unordered_map<const void *, int> g_attr_done;  // kernel -> dynamic smem configured
+
+}  // namespace
+
+void set_error(const std::string &msg) { g_err = msg; }
+tm_status fail(tm_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+
+bool is_specialised(uint64_t code) {
+    for (auto &e : catalog())
+        if (e.code == code) return true;
+    return false;
+}
+
+KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised) {
+    if (mode == kCount || mode == kEnum) {
+        for (auto &e : catalog())
+            if (e.code == code) {
+                if (specialised) *specialised = true;
+                return mode == kCount ? e.count : e.enumerate;
+            }
+    }
+    if (specialised) *specialised = false;
+    switch (mode) {
+        case kCount: return kernel_info<PlanR, kCount>();
+        case kEnum: return kernel_info<PlanR, kEnum>();
+        case kRoots: return kernel_info<PlanR, kRoots>();
+        default: return kernel_info<PlanR, kStats>();
+    }
+}
+
+namespace {
+
+struct RunOut {
+    uint64_t count = 0;
+    uint64_t stats[kScratchWords] = {};
+};
+
+// One query: horizons for δ and every effective δ_i, then the mining kernel.
+tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, int mode, uint32_t *enum_dev,
+              uint64_t cap, const uint64_t *roots_dev, uint64_t n_roots_list, unsigned long long *root_counts_dev,
+              RunOut *out) {
+    if (!g || !mo) return fail(TM_EINVAL, "null graph or motif");
+    tm_run_opts o;
+    tm_run_opts_default(&o);
+    if (opts) o = *opts;
+    DeviceGuard guard(g->device);
+    cudaStream_t s = (cudaStream_t)o.stream;
+    const DeviceGraph &d = g->d;
+    const uint64_t m = d.m;
+    g_info = tm_run_info{};
+
+    MineParams p;
+    std::memset(&p, 0, sizeof p);
+    p.src = d.src; p.dst = d.dst; p.off_out = d.off_out; p.off_in = d.off_in; p.rec = d.rec;
+    p.m = (uint32_t)m;
+    p.L = mo->L;
+    for (uint32_t i = 0; i < mo->L; i++) { p.u[i] = mo->u[i]; p.v[i] = mo->v[i]; }
+    if (roots_dev) {
+        p.roots = roots_dev;
+        p.n_roots = n_roots_list;
+    } else {
+        uint64_t hi = std::min<uint64_t>(o.root_hi, m), lo = std::min<uint64_t>(o.root_lo, hi);
+        p.root_lo = lo;
+        p.n_roots = hi - lo;
+    }
+    if (o.edge_id_offset + m > (1ull << 32)) return fail(TM_EINVAL, "edge_id_offset + m exceeds 2^32");
+    p.id_offset = (uint32_t)o.edge_id_offset;
+    p.enum_buf = enum_dev;
+    p.cap = cap;
+    p.root_counts = root_counts_dev;
+
+    cudaEvent_t ev[4] = {};
+    for (auto &e : ev) TM_CUDA_TRY(cudaEventCreate(&e));
+    struct EvFree { cudaEvent_t *e; ~EvFree() { for (int i = 0; i < 4; i++) if (e[i]) cudaEventDestroy(e[i]); } } evf{ev};
+
+    // distinct horizons: H_δ, and H_{δ_i} for every finite δ_i < δ (a gap
+    // bound >= δ can never bind: t_prev >= t_root).
+    std::vector<int64_t> hv;
+    const bool need_h = mo->L >= 2 && p.n_roots > 0;
+    int gap_buf[kMaxL];
+    if (need_h) {
+        hv.push_back(mo->delta);
+        for (uint32_t i = 0; i + 1 < mo->L; i++) {
+            gap_buf[i] = -1;
+            int64_t f = mo->fine[i];
+            if (f == TM_DELTA_INF || f >= mo->delta) continue;
+            auto it = std::find(hv.begin(), hv.end(), f);
+            gap_buf[i] = (int)(it - hv.begin());
+            if (it == hv.end()) hv.push_back(f);
+        }
+    }
+    unsigned long long *scratch = nullptr;
+    uint32_t *hbuf = nullptr;
+    TM_CUDA_TRY(cudaMallocAsync(&scratch, kScratchWords * sizeof(unsigned long long), s));
+    struct Free { void *a; void *b; cudaStream_t s; ~Free() { if (a) cudaFreeAsync(a, s); if (b) cudaFreeAsync(b, s); } } fr{scratch, nullptr, s};
+    TM_CUDA_TRY(cudaMemsetAsync(scratch, 0, kScratchWords * sizeof(unsigned long long), s));
+    if (need_h) {
+        TM_CUDA_TRY(cudaMallocAsync(&hbuf, hv.size() * m * sizeof(uint32_t), s));
+        fr.b = hbuf;
+    }
+    p.scratch = scratch;
+
+    TM_CUDA_TRY(cudaEventRecord(ev[0], s));
+    for (size_t i = 0; i < hv.size(); i++) {
+        TM_CUDA_TRY(build_horizon(d, hv[i], hbuf + i * m, s));
+        g_info.launches++;
+    }
+    if (need_h) {
+        p.H = hbuf;
+        for (uint32_t i = 0; i + 1 < mo->L; i++) p.Hf[i] = gap_buf[i] >= 0 ? hbuf + (size_t)gap_buf[i] * m : nullptr;
+    }
+    TM_CUDA_TRY(cudaEventRecord(ev[1], s));
+
+    if (p.n_roots > 0) {
+        bool spec = false;
+        KernelInfo ki = lookup_kernel(mo->code, mode, &spec);
+        const int threads = kWarpsPerBlock * 32;
+        const size_t smem = (size_t)ki.smem_per_warp * kWarpsPerBlock;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        {
+            std::lock_guard<std::mutex> lk(g_attr_mu);
+            auto key = (const void *)ki.fn;
+            if (!g_attr_done.count(key)) {
+                TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                g_attr_done[key] = 1;
+            }
+        }
+        int sms = 0, per_sm = 0;
+        TM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        TM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ki.fn, threads, smem));
+        if (per_sm < 1) return fail(TM_ECUDA, "mining kernel does not fit on an SM");
+        uint64_t grid = o.grid_ctas ? o.grid_ctas : (uint64_t)sms * per_sm;
+        // no more warps than 32-root batches
+        uint64_t max_useful = (p.n_roots + 31) / 32;
+        max_useful = (max_useful + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        grid = std::max<uint64_t>(1, std::min(grid, max_useful));
+        ki.fn<<<(unsigned)grid, threads, smem, s>>>(p);
+        TM_CUDA_TRY(cudaGetLastError());
+        g_info.launches++;
+        g_info.grid_ctas = (uint32_t)grid;
+        g_info.block_threads = threads;
+    }
+    TM_CUDA_TRY(cudaEventRecord(ev[2], s));
+    unsigned long long host[kScratchWords];
+    TM_CUDA_TRY(cudaMemcpyAsync(host, scratch, sizeof host, cudaMemcpyDeviceToHost, s));
+    TM_CUDA_TRY(cudaEventRecord(ev[3], s));
+    TM_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaEventElapsedTime(&g_info.horizon_ms, ev[0], ev[1]);
+    cudaEventElapsedTime(&g_info.mine_ms, ev[1], ev[2]);
+    cudaEventElapsedTime(&g_info.total_ms, ev[0], ev[3]);
+    out->count = mode == kEnum ? host[2] : host[1];
+    for (int i = 0; i < kScratchWords; i++) out->stats[i] = host[i];
+    return TM_OK;
+}
+
+tm_status check_graph_args(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m, uint32_t n,
+                           tm_graph **out) {
+    if (!out) return fail(TM_EINVAL, "out is null");
+    *out = nullptr;
+    if (m > TM_MAX_M) return fail(TM_EINVAL, "m exceeds TM_MAX_M (2^31-1)");
+    if (m && (!src || !dst || !t)) return fail(TM_EINVAL, "null edge array");
+    if (m && n == 0) return fail(TM_EINVAL, "n_vertices is 0 but m > 0");
+    return TM_OK;
+}
+
+}  // namespace
+}  // namespace tmg
+
+using namespace tmg;
+
+extern "C" {
+
+const char *tm_last_error(void) { return g_err.c_str(); }
+const char *tm_version(void) { return "tmotif 0.1 (sm_100a)"; }
+
+void tm_run_opts_default(tm_run_opts *o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->root_lo = 0;
+    o->root_hi = UINT64_MAX;
+}
+
+tm_status tm_graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m,
+                          uint32_t n_vertices, const tm_graph_opts *o, tm_graph **out) {
+    g_err.clear();
+    tm_status st = check_graph_args(src, dst, t, m, n_vertices, out);
+    if (st) return st;
+    if (!(o && o->input_on_device)) {  // host input: validate here, cheaply, with exact messages
+        for (uint64_t i = 0; i < m; i++) {
+            if (src[i] >= n_vertices || dst[i] >= n_vertices)
+                return fail(TM_EINVAL, "edge " + std::to_string(i) + ": endpoint >= n_vertices");
+            if (t[i] < 0) return fail(TM_EINVAL, "edge " + std::to_string(i) + ": negative timestamp");
+        }
+    }
+    DeviceGuard guard(o ? o->device : -1);
+    return graph_create(src, dst, t, m, n_vertices, o, out);
+}
+
+tm_status tm_graph_destroy(tm_graph *g) {
+    graph_destroy(g);
+    return TM_OK;
+}
+
+tm_status tm_graph_info(const tm_graph *g, uint64_t *m, uint32_t *n, int *device) {
+    if (!g) return fail(TM_EINVAL, "null graph");
+    if (m) *m = g->d.m;
+    if (n) *n = g->d.n;
+    if (device) *device = g->device;
+    return TM_OK;
+}
+
+tm_status tm_graph_sorted_to_input(const tm_graph *g, uint64_t *perm) {
+    if (!g || (!perm && g->d.m)) return fail(TM_EINVAL, "null argument");
+    DeviceGuard guard(g->device);
+    std::vector<uint32_t> tmp(g->d.m);
+    if (g->d.m) TM_CUDA_TRY(cudaMemcpy(tmp.data(), g->d.perm, g->d.m * 4, cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < g->d.m; i++) perm[i] = tmp[i];
+    return TM_OK;
+}
+
+tm_status tm_graph_sorted_edges(const tm_graph *g, uint32_t *src, uint32_t *dst, int64_t *t) {
+    if (!g) return fail(TM_EINVAL, "null graph");
+    DeviceGuard guard(g->device);
+    const uint64_t m = g->d.m;
+    if (!m) return TM_OK;
+    if (src) TM_CUDA_TRY(cudaMemcpy(src, g->d.src, m * 4, cudaMemcpyDeviceToHost));
+    if (dst) TM_CUDA_TRY(cudaMemcpy(dst, g->d.dst, m * 4, cudaMemcpyDeviceToHost));
+    if (t) TM_CUDA_TRY(cudaMemcpy(t, g->d.t, m * 8, cudaMemcpyDeviceToHost));
+    return TM_OK;
+}
+
+tm_status tm_motif_create(uint32_t L, const uint32_t *mu, const uint32_t *mv, int64_t delta, const int64_t *fine,
+                          tm_motif **out) {
+    g_err.clear();
+    if (!out) return fail(TM_EINVAL, "out is null");
+    *out = nullptr;
+    if (L < 1 || L > TM_MAX_EDGES) return fail(TM_EINVAL, "L must be in 1..TM_MAX_EDGES");
+    if (!mu || !mv) return fail(TM_EINVAL, "null motif edge array");
+    if (delta < 0) return fail(TM_EINVAL, "delta < 0");
+    int label[64];
+    for (int &x : label) x = -1;
+    int nv = 0;
+    tm_motif mo;
+    mo.L = L;
+    mo.delta = delta;
+    for (uint32_t i = 0; i < L; i++) {
+        if (mu[i] >= 64 || mv[i] >= 64) return fail(TM_EINVAL, "motif vertex label >= 64");
+        if (mu[i] == mv[i]) return fail(TM_EINVAL, "motif self-loop");
+        const bool seen_u = label[mu[i]] >= 0, seen_v = label[mv[i]] >= 0;
+        if (i > 0 && !seen_u && !seen_v)
+            return fail(TM_EUNSUPPORTED, "motif edge " + std::to_string(i) +
+                                             " touches no earlier motif vertex (prefix-disconnected, reading Q9)");
+        // relabel by first appearance (u before v)
+        if (!seen_u) label[mu[i]] = nv++;
+        if (!seen_v) label[mv[i]] = nv++;
+        if (nv > TM_MAX_VERTICES) return fail(TM_EINVAL, "more than TM_MAX_VERTICES motif vertices");
+        mo.u[i] = (uint8_t)label[mu[i]];
+        mo.v[i] = (uint8_t)label[mv[i]];
+    }
+    mo.nv = nv;
+    for (int i = 0; i < kMaxL; i++) mo.fine[i] = TM_DELTA_INF;
+    if (fine)
+        for (uint32_t i = 0; i + 1 < L; i++) {
+            if (fine[i] < 0) return fail(TM_EINVAL, "fine delta < 0");
+            mo.fine[i] = fine[i];
+        }
+    mo.code = motif_code((int)L, mo.u, mo.v);
+    tm_motif *p = new (std::nothrow) tm_motif(mo);
+    if (!p) return fail(TM_ENOMEM, "host allocation failed");
+    *out = p;
+    return TM_OK;
+}
+
+tm_status tm_motif_destroy(tm_motif *mo) {
+    delete mo;
+    return TM_OK;
+}
+
+tm_status tm_motif_specialised(const tm_motif *mo, int *sp) {
+    if (!mo || !sp) return fail(TM_EINVAL, "null argument");
+    *sp = is_specialised(mo->code) ? 1 : 0;
+    return TM_OK;
+}
+
+tm_status tm_count(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o, uint64_t *count) {
+    g_err.clear();
+    if (!count) return fail(TM_EINVAL, "count is null");
+    RunOut r;
+    tm_status st = run(g, mo, o, kCount, nullptr, 0, nullptr, 0, nullptr, &r);
+    if (st) return st;
+    *count = r.count;
+    return TM_OK;
+}
+
+tm_status tm_search_stats_run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o, tm_search_stats *out) {
+    g_err.clear();
+    if (!out) return fail(TM_EINVAL, "out is null");
+    RunOut r;
+    tm_status st = run(g, mo, o, kStats, nullptr, 0, nullptr, 0, nullptr, &r);
+    if (st) return st;
+    std::memset(out, 0, sizeof *out);
+    for (int l = 0; l < kMaxL && l < 8; l++) out->nodes[l] = r.stats[kStatsBase + l];
+    // roots that bind motif edge 1 are the level-1 nodes when L >= 2
+    out->window_sum = r.stats[16];
+    out->list_sum = r.stats[17];
+    out->probe_sum = r.stats[18];
+    out->matches = r.count;
+    return TM_OK;
+}
+
+tm_status tm_enumerate(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o, uint32_t *buf, uint64_t cap,
+                       uint64_t *n_total, uint64_t *n_written) {
+    g_err.clear();
+    if (!g || !mo || !n_total) return fail(TM_EINVAL, "null argument");
+    if (cap && !buf) return fail(TM_EINVAL, "buf is null with cap > 0");
+    tm_run_opts opt;
+    tm_run_opts_default(&opt);
+    if (o) opt = *o;
+    DeviceGuard guard(g->device);
+    cudaStream_t s = (cudaStream_t)opt.stream;
+    const uint32_t L = mo->L;
+    uint32_t *dbuf = buf;
+    if (!opt.buffers_on_device && cap) TM_CUDA_TRY(cudaMalloc(&dbuf, cap * L * sizeof(uint32_t)));
+    RunOut r;
+    tm_status st = run(g, mo, &opt, kEnum, dbuf, cap, nullptr, 0, nullptr, &r);
+    const uint64_t written = std::min(r.count, cap);
+    if (st == TM_OK && written && (opt.canonical || !opt.buffers_on_device)) {
+        std::vector<uint32_t> rows(written * L);
+        cudaError_t e = cudaMemcpyAsync(rows.data(), dbuf, written * L * 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = fail(TM_ECUDA, std::string("enumeration copy: ") + cudaGetErrorString(e));
+        if (st == TM_OK && opt.canonical) {
+            std::vector<uint64_t> idx(written);
+            for (uint64_t i = 0; i < written; i++) idx[i] = i;
+            std::sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t b) {
+                return std::lexicographical_compare(&rows[a * L], &rows[a * L + L], &rows[b * L], &rows[b * L + L]);
+            });
+            std::vector<uint32_t> sorted(written * L);
+            for (uint64_t i = 0; i < written; i++) std::memcpy(&sorted[i * L], &rows[idx[i] * L], L * 4);
+            rows.swap(sorted);
+        }
+        if (st == TM_OK) {
+            if (opt.buffers_on_device) {
+                e = cudaMemcpyAsync(dbuf, rows.data(), written * L * 4, cudaMemcpyHostToDevice, s);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                if (e != cudaSuccess) st = fail(TM_ECUDA, std::string("enumeration copy: ") + cudaGetErrorString(e));
+            } else {
+                std::memcpy(buf, rows.data(), written * L * 4);
+            }
+        }
+    }
+    if (!opt.buffers_on_device && cap) cudaFree(dbuf);
+    if (st) return st;
+    *n_total = r.count;
+    if (n_written) *n_written = written;
+    if (r.count > cap) return fail(TM_TRUNCATED, "more matches than buffer rows");
+    return TM_OK;
+}
+
+tm_status tm_count_roots(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o, const uint64_t *roots,
+                         uint64_t n, uint64_t *counts) {
+    g_err.clear();
+    if (!g || !mo || (n && (!roots || !counts))) return fail(TM_EINVAL, "null argument");
+    tm_run_opts opt;
+    tm_run_opts_default(&opt);
+    if (o) opt = *o;
+    if (n == 0) return TM_OK;
+    DeviceGuard guard(g->device);
+    cudaStream_t s = (cudaStream_t)opt.stream;
+    const uint64_t *droots = roots;
+    unsigned long long *dcounts = reinterpret_cast<unsigned long long *>(counts);
+    uint64_t *own_r = nullptr;
+    unsigned long long *own_c = nullptr;
+    if (!opt.buffers_on_device) {
+        for (uint64_t i = 0; i < n; i++)
+            if (roots[i] >= g->d.m) return fail(TM_EINVAL, "root id >= m");
+        TM_CUDA_TRY(cudaMalloc(&own_r, n * 8));
+        TM_CUDA_TRY(cudaMalloc(&own_c, n * 8));
+        TM_CUDA_TRY(cudaMemcpyAsync(own_r, roots, n * 8, cudaMemcpyHostToDevice, s));
+        droots = own_r;
+        dcounts = own_c;
+    }
+    TM_CUDA_TRY(cudaMemsetAsync(dcounts, 0, n * 8, s));
+    RunOut r;
+    tm_status st = run(g, mo, &opt, kRoots, nullptr, 0, droots, n, dcounts, &r);
+    if (st == TM_OK && !opt.buffers_on_device) {
+        cudaError_t e = cudaMemcpyAsync(counts, own_c, n * 8, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = fail(TM_ECUDA, std::string("counts copy: ") + cudaGetErrorString(e));
+    }
+    cudaFree(own_r);
+    cudaFree(own_c);
+    return st;
+}
+
+tm_status tm_last_run_info(tm_run_info *out) {
+    if (!out) return fail(TM_EINVAL, "out is null");
+    *out = g_info;
+    return TM_OK;
+}
+
+tm_status tm_partition_plan(const int64_t *t, uint64_t m, int64_t delta, uint32_t P, const uint64_t *weights,
+                            uint64_t *root_lo, uint64_t *edge_hi) {
+    g_err.clear();
+    if (P == 0 || !root_lo || !edge_hi || (m && !t)) return fail(TM_EINVAL, "bad argument");
+    if (delta < 0) return fail(TM_EINVAL, "delta < 0");
+    for (uint64_t i = 0; i + 1 < m; i++)
+        if (t[i] > t[i + 1]) return fail(TM_EINVAL, "t_sorted is not sorted");
+    auto horizon = [&](uint64_t r) -> uint64_t {  // max{j : t[j] <= t[r] + δ}
+        if (delta == TM_DELTA_INF || t[r] > INT64_MAX - delta) return m - 1;
+        return (uint64_t)(std::upper_bound(t + r, t + m, t[r] + delta) - t) - 1;
+    };
+    std::vector<long double> pre(m + 1, 0.0L);
+    for (uint64_t r = 0; r < m; r++)
+        pre[r + 1] = pre[r] + (long double)(weights ? weights[r] : (horizon(r) - r + 1));
+    root_lo[0] = 0;
+    for (uint32_t q = 1; q < P; q++) {
+        long double target = pre[m] * q / P;
+        uint64_t r = (uint64_t)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+        r = std::min<uint64_t>(std::max<uint64_t>(r, root_lo[q - 1]), m);
+        root_lo[q] = r;
+    }
+    root_lo[P] = m;
+    for (uint32_t q = 0; q < P; q++)
+        edge_hi[q] = root_lo[q + 1] > root_lo[q] ? horizon(root_lo[q + 1] - 1) + 1 : root_lo[q];
+    return TM_OK;
+}
+
+}  // extern "C"

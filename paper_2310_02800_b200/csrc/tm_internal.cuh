@@ -1,0 +1,110 @@
+// Internal declarations of libtmotif (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+#include "../../include/tmotif.h"
+
+namespace tmg {
+
+constexpr int kMaxL = TM_MAX_EDGES;      // motif edges
+constexpr int kMaxV = TM_MAX_VERTICES;   // motif vertices
+
+// Device-resident temporal graph.
+//   src/dst/t : the chronologically sorted temporal edge list; edge
+//               id = rank by (t, input position) (reading Q1).
+//   rec       : 2m packed 64-bit records (edge id << 32 | neighbour):
+//               [0, m) out-adjacency grouped by source, [m, 2m) in-adjacency
+//               grouped by destination; ascending edge id inside each group
+//               = time order.
+//   off_out   : n+1 offsets into rec (values in [0, m]).
+//   off_in    : n+1 offsets into rec, pre-biased by m (values in [m, 2m]).
+//   perm      : perm[id] = input position.
+struct DeviceGraph {
+    uint64_t m = 0;
+    uint32_t n = 0;
+    uint32_t *src = nullptr, *dst = nullptr;
+    int64_t *t = nullptr;
+    uint32_t *perm = nullptr;
+    uint32_t *off_out = nullptr, *off_in = nullptr;
+    uint64_t *rec = nullptr;
+};
+
+}  // namespace tmg
+
+struct tm_graph {
+    int device = 0;
+    tmg::DeviceGraph d;
+};
+
+struct tm_motif {
+    uint32_t L = 0;          // motif edges
+    uint32_t nv = 0;         // motif vertices
+    uint8_t u[tmg::kMaxL] = {}, v[tmg::kMaxL] = {};   // relabelled by first appearance
+    int64_t delta = 0;
+    int64_t fine[tmg::kMaxL] = {};                    // gap i between edges i and i+1 (0-based)
+    uint64_t code = 0;       // packed structure, selects the specialised kernel
+};
+
+namespace tmg {
+
+// Modes of the mining kernel.
+enum Mode : int { kCount = 0, kEnum = 1, kRoots = 2, kStats = 3 };
+
+// Packed motif structure: bits 0-2 L, then per edge i: u at 3+6i, v at 6+6i.
+constexpr uint64_t motif_code(int L, const uint8_t *u, const uint8_t *v) {
+    uint64_t c = (uint64_t)L;
+    for (int i = 0; i < L; i++) c |= ((uint64_t)u[i] << (3 + 6 * i)) | ((uint64_t)v[i] << (6 + 6 * i));
+    return c;
+}
+
+// Kernel parameters of one mining launch (passed by value; lives in the
+// constant bank).
+struct MineParams {
+    const uint32_t *src, *dst;
+    const uint32_t *off_out, *off_in;
+    const uint64_t *rec;
+    uint32_t m;
+    const uint32_t *H;                 // H_δ  (coarse δ-horizon)
+    const uint32_t *Hf[kMaxL];         // H_{δ_i} per gap i, nullptr when δ_i = ∞
+    uint64_t root_lo, n_roots;         // roots root_lo + [0, n_roots) ...
+    const uint64_t *roots;             // ... or roots[0, n_roots) when non-null
+    unsigned long long *scratch;       // [0] root cursor, [1] count, [2] enum cursor, [8..] stats
+    unsigned long long *root_counts;   // kRoots: per root slot
+    uint32_t *enum_buf;
+    uint64_t cap;
+    uint32_t id_offset;
+    // runtime plan (generic kernel)
+    uint32_t L;
+    uint8_t u[kMaxL], v[kMaxL];
+};
+
+constexpr int kScratchWords = 32;
+constexpr int kStatsBase = 8;   // scratch[8 + l] nodes[l], [16] window, [17] list, [18] probes
+
+using MineKernel = void (*)(MineParams);
+
+struct KernelInfo {
+    MineKernel fn;
+    int smem_per_warp;    // bytes
+};
+
+// catalog lookup: specialised kernel for `code` in `mode`, else the generic one
+KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised);
+bool is_specialised(uint64_t code);
+
+// error plumbing
+void set_error(const std::string &msg);
+tm_status fail(tm_status st, const std::string &msg);
+
+}  // namespace tmg
+
+#define TM_CUDA_TRY(expr)                                                                   \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            return tmg::fail(_e == cudaErrorMemoryAllocation ? TM_ENOMEM : TM_ECUDA,          \
+                            std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+    } while (0)

@@ -52,7 +52,7 @@ SPECS = {
     "C1": GraphSpec("C1 tiny", 1000, 20_000, 7 * DAY, 2.0, 1.0, 0.03, 3600.0),
     "C2": GraphSpec("C2 email-Eu-core-shaped", 986, 332_334, 803 * DAY, 13.3, 1.0, 0.03, 600.0, fanout=0.1),
     "C3": GraphSpec("C3 wiki-talk-shaped", 1_140_149, 7_833_140, int(6.24 * YEAR), 2.81, 1.0, 0.01, 3600.0),
-    "C4": GraphSpec("C4 stackoverflow-shaped", 2_601_977, 63_497_050, int(7.6 * YEAR), 1.82, 0.8, 0.003, 3600.0),
+    "C4": GraphSpec("C4 stackoverflow-shaped", 2_601_977, 63_497_050, int(7.6 * YEAR), 1.82, 1.0, 0.003, 3600.0),
 }
 
 
@@ -81,11 +81,10 @@ def generate(spec: GraphSpec, seed: int, *, m: int | None = None, shuffle: bool 
     n = spec.n
     m = spec.m if m is None else m
     p = activity(n, spec.alpha, spec.cap, rng)
-    cdf = np.cumsum(p)
-    cdf[-1] = 1.0
 
     def draw(k):
-        return np.minimum(np.searchsorted(cdf, rng.random(k), side="right"), n - 1).astype(np.int64)
+        # k i.i.d. draws from p: multinomial counts, then a seeded shuffle
+        return rng.permutation(np.repeat(np.arange(n, dtype=np.int64), rng.multinomial(k, p)))
 
     per_session = spec.mu * (1.0 + spec.fanout * 2.5)
     S = int(math.ceil(m / per_session * 1.15)) + 64
@@ -139,7 +138,8 @@ def generate(spec: GraphSpec, seed: int, *, m: int | None = None, shuffle: bool 
     if es.size < m:
         raise RuntimeError(f"generator produced {es.size} < {m} events; raise oversampling")
     es, ed, t = es[:m], ed[:m], t[:m]
-    o = np.argsort(t, kind="stable")            # (t, session, event)
+    # (t, session, event): t < 2^33 and the session-order position < 2^30
+    o = np.sort((t << 30) | np.arange(m, dtype=np.int64)) & ((1 << 30) - 1)
     src = es[o].astype(np.uint32)
     dst = ed[o].astype(np.uint32)
     tt = (t[o] + spec.t0).astype(np.int64)

@@ -1,0 +1,297 @@
+"""Thin ctypes binding of libtmotif.so (C ABI in include/tmotif.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA
+kernels.  Functions keep the C names (``tm_graph_create``, ``tm_count`` ...);
+``Graph``/``Motif`` are small RAII wrappers around the handles.  Buffers may
+be numpy arrays (host) or torch CUDA tensors (device; PyTorch supplies device
+memory and streams only).  There is no CPU fallback: if the library is
+missing this module raises on first use.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtmotif.so")
+
+TM_OK, TM_EINVAL, TM_ENOMEM, TM_ECUDA, TM_EUNSUPPORTED, TM_TRUNCATED = range(6)
+DELTA_INF = (1 << 63) - 1
+MAX_EDGES = 6
+_STATUS = {1: "TM_EINVAL", 2: "TM_ENOMEM", 3: "TM_ECUDA", 4: "TM_EUNSUPPORTED", 5: "TM_TRUNCATED"}
+
+_P = ctypes.c_void_p
+_u64, _u32, _i64, _i32, _f32 = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int64, ctypes.c_int, ctypes.c_float
+
+
+class TMotifError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class GraphOpts(ctypes.Structure):
+    _fields_ = [("device", _i32), ("stream", _P), ("input_on_device", _i32)]
+
+
+class RunOpts(ctypes.Structure):
+    _fields_ = [("stream", _P), ("root_lo", _u64), ("root_hi", _u64), ("edge_id_offset", _u64),
+                ("canonical", _i32), ("buffers_on_device", _i32), ("grid_ctas", _u32),
+                ("block_threads", _u32)]
+
+
+class SearchStats(ctypes.Structure):
+    _fields_ = [("nodes", _u64 * 8), ("window_sum", _u64), ("list_sum", _u64), ("probe_sum", _u64),
+                ("matches", _u64)]
+
+
+class RunInfo(ctypes.Structure):
+    _fields_ = [("horizon_ms", _f32), ("mine_ms", _f32), ("total_ms", _f32), ("launches", _u32),
+                ("grid_ctas", _u32), ("block_threads", _u32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+# (name, restype, argtypes) of every symbol include/tmotif.h declares
+SIGNATURES = [
+    ("tm_graph_create", _i32, [_P, _P, _P, _u64, _u32, ctypes.POINTER(GraphOpts), ctypes.POINTER(_P)]),
+    ("tm_graph_destroy", _i32, [_P]),
+    ("tm_graph_info", _i32, [_P, ctypes.POINTER(_u64), ctypes.POINTER(_u32), ctypes.POINTER(_i32)]),
+    ("tm_graph_sorted_to_input", _i32, [_P, _P]),
+    ("tm_graph_sorted_edges", _i32, [_P, _P, _P, _P]),
+    ("tm_motif_create", _i32, [_u32, _P, _P, _i64, _P, ctypes.POINTER(_P)]),
+    ("tm_motif_destroy", _i32, [_P]),
+    ("tm_motif_specialised", _i32, [_P, ctypes.POINTER(_i32)]),
+    ("tm_run_opts_default", None, [ctypes.POINTER(RunOpts)]),
+    ("tm_count", _i32, [_P, _P, ctypes.POINTER(RunOpts), ctypes.POINTER(_u64)]),
+    ("tm_enumerate", _i32, [_P, _P, ctypes.POINTER(RunOpts), _P, _u64, ctypes.POINTER(_u64),
+                            ctypes.POINTER(_u64)]),
+    ("tm_count_roots", _i32, [_P, _P, ctypes.POINTER(RunOpts), _P, _u64, _P]),
+    ("tm_search_stats_run", _i32, [_P, _P, ctypes.POINTER(RunOpts), ctypes.POINTER(SearchStats)]),
+    ("tm_last_run_info", _i32, [ctypes.POINTER(RunInfo)]),
+    ("tm_partition_plan", _i32, [_P, _u64, _i64, _u32, _P, _P, _P]),
+    ("tm_last_error", ctypes.c_char_p, []),
+    ("tm_version", ctypes.c_char_p, []),
+]
+
+
+def lib():
+    """Load libtmotif.so (raises if it was not built — no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} missing: build it with `python -c 'import __graft_entry__ as g; "
+                                  f"g.build()'` (there is no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH)
+            for name, res, args in SIGNATURES:
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != TM_OK:
+        raise TMotifError(st, lib().tm_last_error().decode())
+
+
+def _is_torch(a):
+    return type(a).__module__.startswith("torch")
+
+
+def _host_ptr(a):
+    return a.ctypes.data_as(_P)
+
+
+def _ptr(a):
+    """Pointer of a numpy array (host) or a torch tensor (its data_ptr())."""
+    if a is None:
+        return None
+    if _is_torch(a):
+        return _P(a.data_ptr())
+    return _host_ptr(a)
+
+
+def _stream_handle(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return _P(stream)
+    return _P(stream.cuda_stream)  # torch.cuda.Stream
+
+
+def run_opts(stream=None, root_range=None, edge_id_offset=0, canonical=False, buffers_on_device=False,
+             grid_ctas=0) -> RunOpts:
+    o = RunOpts()
+    lib().tm_run_opts_default(ctypes.byref(o))
+    o.stream = _stream_handle(stream)
+    if root_range is not None:
+        o.root_lo, o.root_hi = int(root_range[0]), int(root_range[1])
+    o.edge_id_offset = int(edge_id_offset)
+    o.canonical = int(bool(canonical))
+    o.buffers_on_device = int(bool(buffers_on_device))
+    o.grid_ctas = int(grid_ctas)
+    return o
+
+
+# ----------------------------------------------------------------- handles
+class Graph:
+    """tm_graph: device-resident sorted edge list + bidirectional CSR."""
+
+    def __init__(self, src, dst, t, n_vertices: int, *, device: int = -1, stream=None):
+        L = lib()
+        on_dev = _is_torch(src)
+        if on_dev:
+            import torch
+            src = src.to(torch.int32).contiguous()
+            dst = dst.to(torch.int32).contiguous()
+            t = t.to(torch.int64).contiguous()
+            if device < 0:
+                device = src.device.index
+        else:
+            src = np.ascontiguousarray(src, np.uint32)
+            dst = np.ascontiguousarray(dst, np.uint32)
+            t = np.ascontiguousarray(t, np.int64)
+        self._keep = (src, dst, t)
+        m = int(src.shape[0])
+        o = GraphOpts(device, _stream_handle(stream), int(on_dev))
+        h = _P()
+        _check(L.tm_graph_create(_ptr(src), _ptr(dst), _ptr(t), m, int(n_vertices), ctypes.byref(o),
+                                 ctypes.byref(h)))
+        self._keep = None
+        self._h = h
+        mm, nn, dd = _u64(), _u32(), _i32()
+        _check(L.tm_graph_info(h, ctypes.byref(mm), ctypes.byref(nn), ctypes.byref(dd)))
+        self.m, self.n, self.device = int(mm.value), int(nn.value), int(dd.value)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tm_graph_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def sorted_to_input(self) -> np.ndarray:
+        perm = np.empty(self.m, np.uint64)
+        _check(lib().tm_graph_sorted_to_input(self._h, _host_ptr(perm)))
+        return perm
+
+    def sorted_edges(self):
+        s = np.empty(self.m, np.uint32); d = np.empty(self.m, np.uint32); t = np.empty(self.m, np.int64)
+        _check(lib().tm_graph_sorted_edges(self._h, _host_ptr(s), _host_ptr(d), _host_ptr(t)))
+        return s, d, t
+
+
+class Motif:
+    """tm_motif: ordered motif edges + δ + optional per-gap δ_i."""
+
+    def __init__(self, edges, delta: int, fine=None):
+        L = len(edges)
+        mu = np.array([int(e[0]) for e in edges], np.uint32)
+        mv = np.array([int(e[1]) for e in edges], np.uint32)
+        fa = None
+        if fine is not None:
+            fa = np.array([DELTA_INF if f is None else int(f) for f in fine], np.int64)
+            if fa.shape[0] != max(L - 1, 0):
+                raise ValueError("fine needs L-1 entries")
+        h = _P()
+        _check(lib().tm_motif_create(L, _host_ptr(mu), _host_ptr(mv), int(delta),
+                                     None if fa is None else _host_ptr(fa), ctypes.byref(h)))
+        self._h = h
+        self.L = L
+        self.edges = [tuple(e) for e in edges]
+        self.delta = delta
+        self.fine = fine
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def specialised(self) -> bool:
+        s = _i32()
+        _check(lib().tm_motif_specialised(self._h, ctypes.byref(s)))
+        return bool(s.value)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tm_motif_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+# -------------------------------------------------------------- the calls
+def tm_count(g: Graph, mo: Motif, **opts) -> int:
+    c = _u64()
+    o = run_opts(**opts)
+    _check(lib().tm_count(g.handle, mo.handle, ctypes.byref(o), ctypes.byref(c)))
+    return int(c.value)
+
+
+def tm_enumerate(g: Graph, mo: Motif, cap: int, buf=None, **opts):
+    """Returns (rows, n_total).  buf: None (host numpy result), a numpy
+    (cap, L) uint32 array, or a torch CUDA int32 tensor (written in place)."""
+    on_dev = buf is not None and _is_torch(buf)
+    if buf is None:
+        buf = np.zeros((max(cap, 1), mo.L), np.uint32)
+    o = run_opts(buffers_on_device=on_dev, **opts)
+    nt, nw = _u64(), _u64()
+    st = lib().tm_enumerate(g.handle, mo.handle, ctypes.byref(o), _ptr(buf), int(cap), ctypes.byref(nt),
+                            ctypes.byref(nw))
+    if st not in (TM_OK, TM_TRUNCATED):
+        _check(st)
+    return buf[: int(nw.value)], int(nt.value)
+
+
+def tm_count_roots(g: Graph, mo: Motif, roots, **opts):
+    if _is_torch(roots):
+        import torch
+        counts = torch.zeros(roots.shape[0], dtype=torch.int64, device=roots.device)
+        o = run_opts(buffers_on_device=True, **opts)
+    else:
+        roots = np.ascontiguousarray(roots, np.uint64)
+        counts = np.zeros(roots.shape[0], np.uint64)
+        o = run_opts(**opts)
+    _check(lib().tm_count_roots(g.handle, mo.handle, ctypes.byref(o), _ptr(roots), int(roots.shape[0]),
+                                _ptr(counts)))
+    return counts
+
+
+def tm_search_stats_run(g: Graph, mo: Motif, **opts) -> dict:
+    s = SearchStats()
+    o = run_opts(**opts)
+    _check(lib().tm_search_stats_run(g.handle, mo.handle, ctypes.byref(o), ctypes.byref(s)))
+    return {"nodes": list(s.nodes), "window_sum": s.window_sum, "list_sum": s.list_sum,
+            "probe_sum": s.probe_sum, "matches": s.matches}
+
+
+def tm_last_run_info() -> dict:
+    r = RunInfo()
+    _check(lib().tm_last_run_info(ctypes.byref(r)))
+    return {"horizon_ms": r.horizon_ms, "mine_ms": r.mine_ms, "total_ms": r.total_ms, "launches": r.launches,
+            "grid_ctas": r.grid_ctas, "block_threads": r.block_threads}
+
+
+def tm_partition_plan(t_sorted, delta: int, P: int, weights=None):
+    t_sorted = np.ascontiguousarray(t_sorted, np.int64)
+    w = None if weights is None else np.ascontiguousarray(weights, np.uint64)
+    lo = np.zeros(P + 1, np.uint64)
+    hi = np.zeros(P, np.uint64)
+    _check(lib().tm_partition_plan(_host_ptr(t_sorted), int(t_sorted.shape[0]), int(delta), int(P),
+                                   None if w is None else _host_ptr(w), _host_ptr(lo), _host_ptr(hi)))
+    return lo, hi
+
+
+def tm_version() -> str:
+    return lib().tm_version().decode()

@@ -1,0 +1,285 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle, element by
+element on the same seeded inputs.  Everything here is integer work, so the
+bar is bit-exact: counts, per-root counts, canonical-sorted enumerations and
+the search-tree instrumentation counters."""
+from __future__ import annotations
+
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from brute import brute, sorted_edges, verify_match
+from cases import CATALOG, INF, random_fine, random_motif, reverse_prefix_connected
+from golden_io import all_fixtures
+from paper_2310_02800_b200 import motifs as M
+from paper_2310_02800_b200 import synth
+from paper_2310_02800_b200 import tmotif as T
+from pins import census36_sum, time_reverse, two_node_closed_form
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    T.lib()
+
+
+def gpu_rows(g, mo, cap=None):
+    if cap is None:
+        cap = T.tm_count(g, mo)
+    rows, n_total = T.tm_enumerate(g, mo, cap, canonical=True)
+    return [tuple(int(x) for x in r) for r in rows], n_total
+
+
+def check_case(src, dst, t, n, motif, delta, fine, *, rows=True, stats=True, roots=True):
+    og = oracle.Graph(src, dst, t, n)
+    exp = og.mine(motif, delta, fine, enumerate_=rows)
+    g = T.Graph(src, dst, t, n)
+    mo = T.Motif(motif, delta, fine)
+    c = T.tm_count(g, mo)
+    assert c == exp["count"], (motif, delta, fine)
+    if rows:
+        r, n_total = gpu_rows(g, mo)
+        assert n_total == exp["n_total"]
+        assert r == [tuple(int(x) for x in row) for row in exp["rows"]]
+    if stats:
+        st = T.tm_search_stats_run(g, mo)
+        os_ = exp["stats"]
+        assert st["nodes"][:len(motif)] == os_["nodes"][:len(motif)]
+        assert (st["window_sum"], st["list_sum"], st["probe_sum"], st["matches"]) == \
+            (os_["window_sum"], os_["list_sum"], os_["probe_sum"], os_["matches"])
+    if roots and len(src):
+        allr = np.arange(len(src), dtype=np.uint64)
+        pr = og.mine(motif, delta, fine, roots=allr, per_root=True)["per_root"]
+        assert np.array_equal(T.tm_count_roots(g, mo, allr), pr)
+    return c
+
+
+# ------------------------------------------------------------ worked examples
+@pytest.mark.parametrize("fx", all_fixtures(), ids=lambda f: f["name"])
+def test_golden(fx):
+    g = T.Graph(np.array(fx["src"]), np.array(fx["dst"]), np.array(fx["t"]), fx["n"])
+    mo = T.Motif(fx["motif"], fx["delta"], fx["fine"])
+    assert T.tm_count(g, mo) == fx["count"]
+    r, n_total = gpu_rows(g, mo, cap=max(fx["count"], 1))
+    assert n_total == fx["count"] and r == fx["rows"]
+
+
+# -------------------------------------------------- random tiny graphs vs oracle
+@pytest.mark.parametrize("seed", range(8))
+def test_tiny_random_vs_oracle(seed):
+    rng = random.Random(seed)
+    for k in range(25):
+        L = rng.choice([1, 2, 3, 3, 4, 5])
+        motif = rng.choice([c for c in CATALOG if len(c) == L] + [random_motif(rng, L)])
+        src, dst, t, n = synth.tiny_graph(seed * 100 + k, n=rng.randint(2, 9), m=rng.randint(0, 90),
+                                          tmax=rng.choice([5, 30, 200]))
+        delta = rng.choice([0, 3, 10, 25, 100, INF])
+        check_case(src, dst, t, n, motif, delta, random_fine(rng, L))
+
+
+def test_tiny_vs_brute_directly():
+    rng = random.Random(99)
+    for k in range(20):
+        motif = rng.choice(CATALOG)
+        src, dst, t, n = synth.tiny_graph(7000 + k, n=6, m=50, tmax=30)
+        delta = rng.choice([5, 15])
+        g = T.Graph(src, dst, t, n)
+        r, _ = gpu_rows(g, T.Motif(motif, delta))
+        assert r == brute(src, dst, t, motif, delta)
+
+
+def test_six_edge_and_seven_vertex_motifs():
+    rng = random.Random(3)
+    for k in range(10):
+        motif = random_motif(rng, 6, max_v=7)
+        src, dst, t, n = synth.tiny_graph(8000 + k, n=8, m=120, tmax=60)
+        check_case(src, dst, t, n, motif, rng.choice([20, 60]), None)
+
+
+def test_many_windows_spanning_tiles():
+    """Windows longer than a 32-candidate batch, hub vertices, duplicate
+    timestamps: C1-sized graph with a dense hub."""
+    rng = np.random.default_rng(5)
+    m, n = 6000, 40
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    hub = rng.random(m) < 0.3
+    src[hub] = 0
+    t = np.sort(rng.integers(0, 3000, m)).astype(np.int64)
+    for motif in (M.TRI, M.STAR3, M.C4, [(0, 1), (1, 0), (0, 1)], M.TT):
+        check_case(src, dst, t, n, motif, 40, None, rows=len(motif) <= 3)
+        check_case(src, dst, t, n, motif, 40, [10] * (len(motif) - 1), rows=False)
+
+
+# ----------------------------------------------------------------- edge cases
+def test_edge_cases():
+    e = np.zeros(0, np.uint32)
+    g = T.Graph(e, e, np.zeros(0, np.int64), 4)
+    assert T.tm_count(g, T.Motif(M.TRI, 10)) == 0
+    rows, nt = T.tm_enumerate(g, T.Motif(M.TRI, 10), 4)
+    assert nt == 0 and len(rows) == 0
+    # all self-loops
+    g = T.Graph(np.array([1, 1, 2]), np.array([1, 1, 2]), np.array([0, 1, 2]), 3)
+    assert T.tm_count(g, T.Motif([(0, 1)], 10)) == 0
+    # single edge motif = non-self-loop edges; root range restriction
+    src, dst, t, n = synth.tiny_graph(1, n=5, m=300, tmax=100, p_self=0.2)
+    g = T.Graph(src, dst, t, n)
+    assert T.tm_count(g, T.Motif([(0, 1)], 0)) == int(np.sum(src != dst))
+    S, D, _, _ = sorted_edges(src, dst, t)
+    assert T.tm_count(g, T.Motif([(0, 1)], 0), root_range=(10, 50)) == sum(S[i] != D[i] for i in range(10, 50))
+    assert T.tm_count(g, T.Motif(M.TRI, 30), root_range=(300, 400)) == 0
+    # truncated enumeration: exact total, TM_TRUNCATED swallowed by the binding
+    mo = T.Motif(M.TRI, 50)
+    full = T.tm_count(g, mo)
+    assert full > 4
+    rows, nt = T.tm_enumerate(g, mo, 3)
+    assert nt == full and len(rows) == 3
+    Sx, Dx, Tx, _ = sorted_edges(src, dst, t)
+    assert all(verify_match(Sx, Dx, Tx, M.TRI, 50, None, tuple(int(x) for x in r)) for r in rows)
+    # δ = ∞ with fine bounds only
+    check_case(src[:80], dst[:80], t[:80], n, M.C4, INF, [7, 7, 7], rows=False)
+
+
+def test_sorted_view_and_input_order():
+    src, dst, t, n = synth.tiny_graph(12, n=6, m=200, tmax=40)
+    g = T.Graph(src, dst, t, n)
+    S, D, Tt, order = sorted_edges(src, dst, t)
+    s2, d2, t2 = g.sorted_edges()
+    assert list(s2) == S and list(d2) == D and list(t2) == Tt
+    assert list(g.sorted_to_input()) == order
+
+
+def test_device_input_and_device_buffers():
+    import torch
+    src, dst, t, n = synth.config_graph("C1")
+    dev = torch.device("cuda:0")
+    g = T.Graph(torch.from_numpy(src.astype(np.int32)).to(dev), torch.from_numpy(dst.astype(np.int32)).to(dev),
+                torch.from_numpy(t).to(dev), n)
+    mo = T.Motif(M.TRI, 3600)
+    exp = oracle.Graph(src, dst, t, n).mine(M.TRI, 3600, enumerate_=True)
+    s = torch.cuda.Stream()
+    assert T.tm_count(g, mo, stream=s) == exp["count"]
+    buf = torch.zeros((exp["count"], 3), dtype=torch.int32, device=dev)
+    rows, nt = T.tm_enumerate(g, mo, exp["count"], buf=buf, canonical=True)
+    assert nt == exp["count"]
+    assert np.array_equal(buf.cpu().numpy().astype(np.uint32), exp["rows"])
+    roots = torch.arange(0, len(src), 7, dtype=torch.int64, device=dev)
+    pr = T.tm_count_roots(g, mo, roots)
+    opr = oracle.Graph(src, dst, t, n).mine(M.TRI, 3600, roots=np.arange(0, len(src), 7, dtype=np.uint64),
+                                            per_root=True)["per_root"]
+    assert np.array_equal(pr.cpu().numpy().astype(np.uint64), opr)
+
+
+def test_shuffled_input_sorts_stably():
+    src, dst, t, n = synth.config_graph("C1", shuffle=True)
+    check_case(src, dst, t, n, M.TRI, 3600, None, roots=False)
+
+
+# --------------------------------------------------------------- configs
+def test_C1_count_and_enumerate():
+    src, dst, t, n = synth.config_graph("C1")
+    check_case(src, dst, t, n, M.TRI, 3600, None)
+
+
+def test_C2_all_36_and_closed_forms():
+    src, dst, t, n = synth.config_graph("C2")
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    counts = []
+    for name in M.CONFIG_MOTIFS["C2"]:
+        mo = M.get(name)
+        c = T.tm_count(g, T.Motif(mo, 3600))
+        assert c == og.mine(mo, 3600)["count"], name
+        counts.append(c)
+    # invariants computed on the GPU alone, on a sub-graph the pure-Python
+    # closed forms can evaluate
+    s, d, tt = src[:4000], dst[:4000], t[:4000]
+    gs = T.Graph(s, d, tt, n)
+    assert sum(T.tm_count(gs, T.Motif(mm, 3600)) for mm in M.TWO_NODE) == two_node_closed_form(s, d, tt, 3600)
+    s, d, tt = src[:1500], dst[:1500], t[:1500]
+    gs = T.Graph(s, d, tt, n)
+    assert sum(T.tm_count(gs, T.Motif(mm, 600)) for mm in M.P36) == census36_sum(s, d, tt, 600)
+
+
+def test_C3_counts_vs_oracle():
+    src, dst, t, n = synth.config_graph("C3")
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    for name in M.CONFIG_MOTIFS["C3"]:
+        mo = M.get(name)
+        assert T.tm_count(g, T.Motif(mo, 86400)) == og.mine(mo, 86400)["count"], name
+
+
+def test_C3_enumeration_full():
+    src, dst, t, n = synth.config_graph("C3")
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    mo = T.Motif(M.C4, 86400)
+    exp = og.mine(M.C4, 86400, enumerate_=True)
+    r, nt = gpu_rows(g, mo)
+    assert nt == exp["n_total"]
+    assert np.array_equal(np.array(r, np.uint32).reshape(-1, 4), exp["rows"])
+
+
+def test_C4_full_size_sampled_roots_and_symmetry():
+    """BASELINE config C4 at full size in the launch configuration bench.py
+    times: per-root counts of 2^14 sampled roots vs the oracle, the full
+    counts vs a time-reversed + direction-reversed copy of the graph."""
+    src, dst, t, n = synth.config_graph("C4")
+    g = T.Graph(src, dst, t, n)
+    og = oracle.Graph(src, dst, t, n)
+    rng = np.random.default_rng(0)
+    roots = np.sort(rng.choice(len(src), 1 << 14, replace=False)).astype(np.uint64)
+    full = {}
+    for name in M.CONFIG_MOTIFS["C4"]:
+        mot = M.get(name)
+        fine = [21600] * (len(mot) - 1)
+        mo = T.Motif(mot, 86400, fine)
+        pr = T.tm_count_roots(g, mo, roots)
+        assert np.array_equal(pr, og.mine(mot, 86400, fine, roots=roots, per_root=True)["per_root"]), name
+        full[name] = T.tm_count(g, mo)
+        # the sampled roots' counts agree with the count over the same roots in the timed kernel
+    # time + direction reversal of the whole graph (sorted ids reversed)
+    S, D, Tt = g.sorted_edges()
+    C = int(Tt.max())
+    gr = T.Graph(S[::-1].copy(), D[::-1].copy(), (C - Tt[::-1]).copy(), n)
+    for name in M.CONFIG_MOTIFS["C4"]:
+        mot = M.get(name)
+        if not reverse_prefix_connected(mot):
+            continue
+        fine = [21600] * (len(mot) - 1)
+        assert T.tm_count(gr, T.Motif(list(reversed(mot)), 86400, fine)) == full[name], name
+
+
+def test_partition_slices_sum_to_full_count():
+    """Multi-GPU plan exercised on one GPU: each rank's slice [lo, edge_hi)
+    mined for its roots only sums to the unpartitioned count."""
+    src, dst, t, n = synth.config_graph("C3")
+    g = T.Graph(src, dst, t, n)
+    S, D, Tt = g.sorted_edges()
+    for mot, delta in ((M.TRI, 86400), (M.C4, 86400)):
+        total = T.tm_count(g, T.Motif(mot, delta))
+        for P in (2, 3, 8):
+            lo, hi = T.tm_partition_plan(Tt, delta, P)
+            s = 0
+            for p in range(P):
+                a, b, e = int(lo[p]), int(lo[p + 1]), int(hi[p])
+                gp = T.Graph(S[a:e], D[a:e], Tt[a:e], n)
+                s += T.tm_count(gp, T.Motif(mot, delta), root_range=(0, b - a))
+            assert s == total
+
+
+def test_generic_and_specialised_kernels_agree():
+    src, dst, t, n = synth.config_graph("C1")
+    g = T.Graph(src, dst, t, n)
+    allr = np.arange(len(src), dtype=np.uint64)
+    for mot in (M.TRI, M.TT, M.DIA, M.P36[7]):
+        mo = T.Motif(mot, 3600)
+        assert mo.specialised
+        assert T.tm_count(g, mo) == int(T.tm_count_roots(g, mo, allr).sum())  # roots mode = generic kernel
