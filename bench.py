@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the δ-temporal-motif hot path on B200 (BASELINE.json metric:
+root edges/s and motif matches/s at 1/2/4/8 B200; % of HBM peak).
+
+Workload (BASELINE.json config 4, the one the metric's 1/2/4/8-GPU scaling is
+quoted on): stackoverflow-shaped synthetic temporal graph, n = 2,601,977,
+m = 63,497,050 (Table 3), motifs P3, TRI, C4 (4-cycle), DIA
+(5 edges) with δ = 1 day and a per-edge inter-event bound δ_i = 6 h on every
+gap, counting.  One *step* = the four queries over every root edge, each
+rebuilding its δ-horizons (query-time work) and running the mining kernel.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU: ranks take contiguous,
+work-balanced root ranges with their forward δ-halo (tm_partition_plan,
+P:1020-1040), mine them with no inter-GPU traffic, and one NCCL all-reduce
+combines the counts.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2310_02800_b200 import motifs as M  # noqa: E402
+from paper_2310_02800_b200 import synth  # noqa: E402
+
+CONFIG = "C4"
+MOTIFS = ["P3", "TRI", "C4", "DIA"]
+DELTA = 86400
+FINE = 21600
+METRIC = "root edges/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def workload_config(world):
+    spec = synth.SPECS[CONFIG]
+    return {"workload": f"{CONFIG} {spec.name.split(' ', 1)[1]} synthetic temporal graph (BASELINE.json configs[3])",
+            "n": spec.n, "m": spec.m, "motifs": MOTIFS, "delta_s": DELTA, "fine_delta_s": FINE,
+            "mode": "count", "generator": {"alpha": spec.alpha, "cap": spec.cap, "mu": spec.mu, "beta_s": spec.beta,
+                                           "seed": synth.SEED_BASE + 3},
+            "partition": f"{world} contiguous root ranges + forward δ-halo" if world > 1 else "whole graph",
+            "cache": "graph 2.3 GB > 126 MB L2; L2 flushed (256 MiB write) between timed steps"}
+
+
+def motif_fine(name):
+    mot = M.get(name)
+    return mot, [FINE] * (len(mot) - 1)
+
+
+def balgo_bytes(stats, n_roots, L, fine=True):
+    """Algorithmic bytes of one query: what the
+    search must read at least, counted by the method's own instrumentation
+    (tm_search_stats_run), independent of sector granularity and caching:
+      12 B per root           SRC[r], DST[r], H_δ[r]
+      per search node 20 B    list end OFF[x+1] 4, window start rank[e_a] 4,
+                              H_δi[e_prev] 4, the record that ends the window 8
+      8 B per candidate record in the scanned windows."""
+    nodes = sum(stats["nodes"][1:L])
+    return 12 * n_roots + (20 if fine else 16) * nodes + 8 * stats["fast_window_sum"]
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.p = None
+        return self
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        sm, mx, reasons, under = [], 0.0, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                s, m_ = float(f[0]), float(f[1])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx = max(mx, m_)
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+            under.append(s)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        d = json.load(open(PEAKS_PATH))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ oracle
+def oracle_sample(src, dst, t, n, budget_s, seed=0):
+    """The oracle (Algorithm 1 in plain C, OpenMP over roots) as it stands,
+    on all host cores, on a seeded uniform sample of roots of the same
+    workload, sized to ~budget_s of CPU work.  Returns root edges/s etc."""
+    import oracle
+    threads = os.cpu_count() or 1
+    og = oracle.Graph(src, dst, t, n)
+    m = len(src)
+    rng = np.random.default_rng(seed)
+    k = 1 << 14
+    spent, roots_done, matches, t_total = 0.0, 0, 0, 0.0
+    while True:
+        roots = np.sort(rng.choice(m, min(k, m), replace=False)).astype(np.uint64)
+        t0 = time.perf_counter()
+        for name in MOTIFS:
+            mot, fine = motif_fine(name)
+            matches += og.mine(mot, DELTA, fine, roots=roots, threads=threads)["count"]
+        dt = time.perf_counter() - t0
+        t_total += dt
+        roots_done += len(roots) * len(MOTIFS)
+        if t_total >= budget_s or k >= m:
+            break
+        k = int(min(m, k * max(2.0, min(8.0, (budget_s - t_total) / max(dt, 1e-3)))))
+    return {"value": roots_done / t_total, "unit": "root edges/s", "cores": threads, "kind": "oracle",
+            "sample": f"{roots_done // len(MOTIFS)} uniformly sampled roots (seeded) x {len(MOTIFS)} motifs of the "
+                      f"{CONFIG} workload, {t_total:.1f} s on {threads} threads",
+            "matches_per_s": matches / t_total}
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, same config/metric."""
+    src, dst, t, n = synth.config_graph(CONFIG)
+    import oracle
+    threads = os.cpu_count() or 1
+    og = oracle.Graph(src, dst, t, n)
+    m = len(src)
+    per_step = 1 << 18
+    rng = np.random.default_rng(1)
+
+    def step():
+        roots = np.sort(rng.choice(m, per_step, replace=False)).astype(np.uint64)
+        c = 0
+        for name in MOTIFS:
+            mot, fine = motif_fine(name)
+            c += og.mine(mot, DELTA, fine, roots=roots, threads=threads)["count"]
+        return c
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    matches = 0
+    for _ in range(args.steps):
+        matches += step()
+    dt = time.perf_counter() - t0
+    roots = per_step * len(MOTIFS) * args.steps
+    v = roots / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "root edges/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1000 / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i64",
+            "data": "synthetic", "config": workload_config(1), "matches_per_s": matches / dt,
+            "cpu_baseline": {"value": v, "unit": "root edges/s", "cores": threads, "kind": "oracle",
+                             "sample": f"each step {per_step} uniformly sampled roots x {len(MOTIFS)} motifs"},
+            "e2e": {"value": v, "unit": "root edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------- ours
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2310_02800_b200 import tmotif as T
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    t0 = time.time()
+    src, dst, t, n = synth.config_graph(CONFIG)
+    m = len(src)
+    log(f"[rank {rank}] generated {CONFIG}: m={m} n={n} in {time.time() - t0:.1f}s")
+    # contiguous root ranges balanced by the δ-window proxy, + forward δ-halo
+    if world > 1:
+        lo, hi = T.tm_partition_plan(t, DELTA, world)
+        a, b, e = int(lo[rank]), int(lo[rank + 1]), int(hi[rank])
+    else:
+        a, b, e = 0, m, m
+    s_src, s_dst, s_t = (np.ascontiguousarray(x[a:e]) for x in (src, dst, t))
+    stream = torch.cuda.Stream(dev)
+    g = T.Graph(s_src, s_dst, s_t, n, device=local, stream=stream)
+    motifs = [T.Motif(*motif_fine(name)[:1], DELTA, motif_fine(name)[1]) for name in MOTIFS]
+    rr = (0, b - a)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        cs, mine, launches = [], [], 0
+        for mo in motifs:
+            cs.append(T.tm_count(g, mo, root_range=rr, stream=stream))
+            info = T.tm_last_run_info()
+            mine.append(info["mine_ms"])
+            launches += info["launches"]
+        return cs, mine, launches
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, mine_ms, launches, counts = [], np.zeros(len(MOTIFS)), 0, None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()                      # untimed L2 flush between steps
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            cs, mm, nl = step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            mine_ms += np.array(mm)
+            launches += nl
+            counts = cs
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = float(sum(step_ms))
+    ct = torch.tensor(counts, dtype=torch.int64, device=dev)
+    tm_ = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ct, op=dist.ReduceOp.SUM)       # the one exchange: combine the counts
+        dist.all_reduce(tm_, op=dist.ReduceOp.MAX)      # max over ranks
+    total_ms = float(tm_.item())
+    counts = [int(x) for x in ct.tolist()]
+    roots_per_step = m * len(MOTIFS)
+    value = roots_per_step * args.steps / (total_ms / 1000)
+    matches_per_s = sum(counts) * args.steps / (total_ms / 1000)
+
+    # ---- roofline of the dominant kernel (untimed instrumentation runs)
+    bytes_q, per_motif = [], []
+    for i, (name, mo) in enumerate(zip(MOTIFS, motifs)):
+        st = T.tm_search_stats_run(g, mo, root_range=rr, stream=stream)
+        L = len(M.get(name))
+        bq = balgo_bytes(st, b - a, L)
+        bytes_q.append(bq)
+        avg_ms = mine_ms[i] / args.steps
+        per_motif.append({"motif": name, "count": counts[i], "mine_ms": avg_ms,
+                          "alg_bytes": bq, "alg_GBps": bq / (avg_ms / 1000) / 1e9,
+                          "search_nodes": sum(st["nodes"][1:L]), "window_sum": st["window_sum"]})
+    dom = int(np.argmax(mine_ms))
+    peak, peak_src = peaks()
+    dom_ms = mine_ms[dom] / args.steps
+    achieved = bytes_q[dom] / (dom_ms / 1000) / 1e9
+    traffic = None
+    try:
+        nc = json.load(open(NCU_SUMMARY))
+        if nc.get("config") == CONFIG and nc.get("motif") == MOTIFS[dom] and world == 1:
+            traffic = nc.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": f"mine_kernel<PlanC<{MOTIFS[dom]}>, kCount>",
+                "peak_source": peak_src, "per_motif": per_motif,
+                "mine_share_of_step": float(mine_ms.sum() / sum(step_ms))}
+
+    # ---- end to end through the public API from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        ph = [torch.from_numpy(x).pin_memory() for x in (s_src, s_dst, s_t)]
+        hs, hd, ht = (x.numpy() for x in ph)
+
+        def e2e_step():
+            gg = T.Graph(hs, hd, ht, n, device=local, stream=stream)
+            cs = [T.tm_count(gg, mo, root_range=rr, stream=stream) for mo in motifs]
+            gg.close()
+            return cs
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ee = []
+        for _ in range(args.e2e_steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_step()
+            e1.record(stream)
+            e1.synchronize()
+            ee.append(e0.elapsed_time(e1))
+        te = torch.tensor([sum(ee)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": roots_per_step * args.e2e_steps / (float(te.item()) / 1000), "unit": "root edges/s",
+               "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in ph)) * world,
+               "d2h_bytes_per_step": 256 * len(MOTIFS) * world,
+               "includes": "graph load from pinned host (H2D + validate + sort + CSR build) + 4 queries + count read-back"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(src, dst, t, n, args.cpu_seconds)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "root edges/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "config": workload_config(world), "matches_per_s": matches_per_s, "counts": dict(zip(MOTIFS, counts)),
+                "hbm_pct_of_peak": roofline["frac"] * 100, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk.summary(), "gpu_launches": int(launches) * world,
+                "gpu_launches_note": "per rank: H_δ + H_δi horizon kernels and one mining kernel per query"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

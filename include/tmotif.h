@@ -157,13 +157,16 @@ tm_status tm_count_roots(const tm_graph *g, const tm_motif *mo, const tm_run_opt
  * whose candidate window for motif edge l+1 was searched (each exactly once,
  * the P:719-723 candidate-caching invariant); window_sum: Σ window sizes;
  * list_sum: Σ lengths of the adjacency lists searched; probe_sum: Σ
- * ceil(log2(len+1)); matches. */
+ * ceil(log2(len+1)); matches; fast_window_sum: Σ window sizes of the lists
+ * the production kernels actually scan (they may pick the other list of a
+ * both-mapped motif edge), the basis of the algorithmic bytes. */
 typedef struct {
     uint64_t nodes[8];
     uint64_t window_sum;
     uint64_t list_sum;
     uint64_t probe_sum;
     uint64_t matches;
+    uint64_t fast_window_sum;
 } tm_search_stats;
 
 tm_status tm_search_stats_run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o,

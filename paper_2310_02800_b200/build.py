@@ -26,7 +26,10 @@ def _needs(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, jobs: int | None = None, extra_flags=()) -> str:
+def build(verbose: bool = False, jobs: int | None = None, extra_flags=(), lib: str = LIB, obj: str = OBJ) -> str:
+    """extra_flags/lib/obj build a tuning variant (e.g. -DTM_MIN_BLOCKS=8) into another path."""
+    global OBJ, LIB
+    OBJ, LIB = obj, lib
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(HERE, "..", "include", "*.h"))
@@ -64,4 +67,13 @@ def build(verbose: bool = False, jobs: int | None = None, extra_flags=()) -> str
 
 
 if __name__ == "__main__":
-    print(build(verbose=True))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--variant", default=None, help="name of a tuning variant (built under variants/)")
+    ap.add_argument("flags", nargs="*", help="extra nvcc flags, e.g. -DTM_MIN_BLOCKS=8")
+    a = ap.parse_args()
+    if a.variant:
+        vd = os.path.join(HERE, "..", "variants", a.variant)
+        print(build(verbose=True, extra_flags=a.flags, lib=os.path.join(vd, "libtmotif.so"), obj=os.path.join(vd, "obj")))
+    else:
+        print(build(verbose=True, extra_flags=a.flags))

@@ -14,7 +14,8 @@ namespace tmg {
 tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m, uint32_t n,
                        const tm_graph_opts *o, tm_graph **out);
 void graph_destroy(tm_graph *g);
-cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, cudaStream_t s);
+cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, uint64_t *scratch, cudaStream_t s);
+size_t horizon_scratch_words(uint64_t m);
 
 namespace {
 thread_local std::string g_err;
@@ -104,7 +105,7 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
 
     MineParams p;
     std::memset(&p, 0, sizeof p);
-    p.src = d.src; p.dst = d.dst; p.off_out = d.off_out; p.off_in = d.off_in; p.rec = d.rec;
+    p.src = d.src; p.dst = d.dst; p.off_out = d.off_out; p.off_in = d.off_in; p.rec = d.rec; p.rank = d.rank;
     p.m = (uint32_t)m;
     p.L = mo->L;
     for (uint32_t i = 0; i < mo->L; i++) { p.u[i] = mo->u[i]; p.v[i] = mo->v[i]; }
@@ -145,18 +146,21 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     unsigned long long *scratch = nullptr;
     uint32_t *hbuf = nullptr;
     TM_CUDA_TRY(cudaMallocAsync(&scratch, kScratchWords * sizeof(unsigned long long), s));
-    struct Free { void *a; void *b; cudaStream_t s; ~Free() { if (a) cudaFreeAsync(a, s); if (b) cudaFreeAsync(b, s); } } fr{scratch, nullptr, s};
+    struct Free { void *a; void *b; void *c; cudaStream_t s; ~Free() { if (a) cudaFreeAsync(a, s); if (b) cudaFreeAsync(b, s); if (c) cudaFreeAsync(c, s); } } fr{scratch, nullptr, nullptr, s};
     TM_CUDA_TRY(cudaMemsetAsync(scratch, 0, kScratchWords * sizeof(unsigned long long), s));
+    uint64_t *hscr = nullptr;
     if (need_h) {
         TM_CUDA_TRY(cudaMallocAsync(&hbuf, hv.size() * m * sizeof(uint32_t), s));
         fr.b = hbuf;
+        TM_CUDA_TRY(cudaMallocAsync(&hscr, horizon_scratch_words(m) * sizeof(uint64_t), s));
+        fr.c = hscr;
     }
     p.scratch = scratch;
 
     TM_CUDA_TRY(cudaEventRecord(ev[0], s));
     for (size_t i = 0; i < hv.size(); i++) {
-        TM_CUDA_TRY(build_horizon(d, hv[i], hbuf + i * m, s));
-        g_info.launches++;
+        TM_CUDA_TRY(build_horizon(d, hv[i], hbuf + i * m, hscr, s));
+        g_info.launches += 2;
     }
     if (need_h) {
         p.H = hbuf;
@@ -176,6 +180,10 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
             auto key = (const void *)ki.fn;
             if (!g_attr_done.count(key)) {
                 TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+#ifdef TM_CARVEOUT_MAX
+                TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                 (int)cudaSharedmemCarveoutMaxShared));
+#endif
                 g_attr_done[key] = 1;
             }
         }
@@ -239,7 +247,7 @@ tm_status tm_graph_create(const uint32_t *src, const uint32_t *dst, const int64_
     g_err.clear();
     tm_status st = check_graph_args(src, dst, t, m, n_vertices, out);
     if (st) return st;
-    if (!(o && o->input_on_device)) {  // host input: validate here, cheaply, with exact messages
+    if (!(o && o->input_on_device) && m <= (1u << 20)) {  // small host input: exact messages here; the device check covers the rest
         for (uint64_t i = 0; i < m; i++) {
             if (src[i] >= n_vertices || dst[i] >= n_vertices)
                 return fail(TM_EINVAL, "edge " + std::to_string(i) + ": endpoint >= n_vertices");
@@ -358,6 +366,7 @@ tm_status tm_search_stats_run(const tm_graph *g, const tm_motif *mo, const tm_ru
     out->window_sum = r.stats[16];
     out->list_sum = r.stats[17];
     out->probe_sum = r.stats[18];
+    out->fast_window_sum = r.stats[19];
     out->matches = r.count;
     return TM_OK;
 }

@@ -45,31 +45,116 @@ __global__ void k_bias(uint32_t *off, uint32_t n1, uint32_t bias) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n1; i += gridDim.x * blockDim.x) off[i] += bias;
 }
 
-// records of one direction: edge ids grouped by key vertex, ascending id
-__global__ void k_records(const uint32_t *ids, const uint32_t *nbr, uint64_t m, uint64_t *rec) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t e = ids[i];
-        rec[i] = ((uint64_t)e << 32) | nbr[e];
-    }
-}
-
 // H_d[e] = max{ j : T[j] <= T[e] + d }  (>= e; m-1 when d = ∞ or saturated).
 // The δ-window t' = t_root + δ of Algorithm 1 and the
 // fine-grained bound t_prev + δ_i become edge-id limits.
-__global__ void k_horizon(const int64_t *__restrict__ T, uint64_t m, int64_t d, uint32_t *__restrict__ H) {
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
-        const int64_t te = T[e];
-        if (d == TM_DELTA_INF || te > INT64_MAX - d) { H[e] = (uint32_t)(m - 1); continue; }
-        const int64_t key = te + d;
-        // gallop from e, then binary search: first j > e with T[j] > key
-        uint64_t lo = e + 1, step = 1, hi = e + 1;
-        while (hi < m && T[hi] <= key) { lo = hi + 1; hi = e + 1 + (step <<= 1) - 1; }
-        if (hi > m) hi = m;
-        while (lo < hi) {
-            uint64_t mid = lo + ((hi - lo) >> 1);
-            if (T[mid] > key) hi = mid; else lo = mid + 1;
+// H is monotone, so a block of kHB consecutive edges has all its answers in
+// [H(e0), H(e_last)]: two threads find those ends in global memory, the
+// block stages T over that range in shared memory (coalesced) and every
+// thread binary-searches there.  Bursty stretches whose range exceeds the
+// stage fall back to a per-thread gallop in global memory.
+constexpr int kHB = 512;       // edges per block
+constexpr int kHStage = 3072;  // staged timestamps (24 KB)
+
+__device__ __forceinline__ uint64_t horizon_one(const int64_t *__restrict__ T, uint64_t m, int64_t d, uint64_t e) {
+    const int64_t te = T[e];
+    if (d == TM_DELTA_INF || te > INT64_MAX - d) return m - 1;
+    const int64_t key = te + d;
+    uint64_t lo = e + 1, step = 1, hi;
+    while (true) {       // gallop from e, then binary search: first j > e with T[j] > key
+        hi = lo + step - 1;
+        if (hi >= m) { hi = m; break; }
+        if (T[hi] > key) break;
+        lo = hi + 1;
+        step <<= 1;
+    }
+    while (lo < hi) {
+        uint64_t mid = lo + ((hi - lo) >> 1);
+        if (T[mid] > key) hi = mid; else lo = mid + 1;
+    }
+    return lo - 1;
+}
+
+// H at the first and last edge of every kHB block (one thread each)
+__global__ void k_horizon_ends(const int64_t *__restrict__ T, uint64_t m, int64_t d, uint64_t *__restrict__ ends) {
+    const uint64_t nb = (m + kHB - 1) / kHB;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 2 * nb; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = i >> 1;
+        const uint64_t e = (i & 1) ? min((b + 1) * kHB, m) - 1 : b * kHB;
+        ends[i] = horizon_one(T, m, d, e);
+    }
+}
+
+__global__ void __launch_bounds__(kHB) k_horizon(const int64_t *__restrict__ T, uint64_t m, int64_t d,
+                                                 const uint64_t *__restrict__ ends, uint32_t *__restrict__ H) {
+    __shared__ int64_t st[kHStage];
+    const uint64_t e0 = (uint64_t)blockIdx.x * kHB;
+    const uint64_t e = e0 + threadIdx.x;
+    const uint64_t elast = min(e0 + kHB, m) - 1;
+    const uint64_t lo = ends[2 * blockIdx.x], hi = ends[2 * blockIdx.x + 1];   // answers lie in [lo, hi]
+    const uint64_t span = hi - lo + 1;
+    if (span <= kHStage) {
+        for (uint64_t i = threadIdx.x; i < span; i += kHB) st[i] = T[lo + i];
+        __syncthreads();
+        if (e <= elast) {
+            const int64_t te = T[e];
+            uint64_t r;
+            if (d == TM_DELTA_INF || te > INT64_MAX - d) {
+                r = m - 1;
+            } else {
+                const int64_t key = te + d;   // st[0] = T[H(e0)] <= key
+                uint32_t a = 0, b = (uint32_t)span;
+                while (a < b) {
+                    uint32_t mid = (a + b) >> 1;
+                    if (st[mid] > key) b = mid; else a = mid + 1;
+                }
+                r = lo + a - 1;
+            }
+            H[e] = (uint32_t)r;
         }
-        H[e] = (uint32_t)(lo - 1);
+    } else if (e <= elast) {
+        H[e] = (uint32_t)horizon_one(T, m, d, e);
+    }
+}
+
+// Both CSR directions and the rank arrays from one stable sort of the 2m
+// (vertex, edge) incidences: entry 2e is e's out-incidence at src(e), entry
+// 2e+1 its in-incidence at dst(e).  A stable sort by vertex lists, for every
+// vertex, all edges touching it in id (= time) order; a scan of "is an
+// out-incidence" flags then counts, at every entry, the out- and in-edges of
+// that vertex that come earlier — exactly the list positions and the ranks.
+__global__ void k_incidences(const uint32_t *src, const uint32_t *dst, uint64_t m, uint32_t *key, uint32_t *val) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 2 * m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t e = i >> 1;
+        key[i] = (i & 1) ? dst[e] : src[e];
+        val[i] = (uint32_t)i;
+    }
+}
+
+__global__ void k_outflag(const uint32_t *val, uint64_t n2, uint32_t *flag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n2; i += (uint64_t)gridDim.x * blockDim.x)
+        flag[i] = (val[i] & 1u) ? 0u : 1u;
+}
+
+__global__ void k_scatter_csr(const uint32_t *key, const uint32_t *val, const uint32_t *outb, const uint32_t *src,
+                              const uint32_t *dst, const uint32_t *off_out, const uint32_t *off_in, uint64_t m,
+                              uint64_t *rec, uint32_t *rank) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 2 * m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = key[i], ent = val[i], e = ent >> 1;
+        const uint64_t seg = (uint64_t)off_out[v] + (off_in[v] - m);   // first incidence of v
+        const uint32_t ob = outb[i] - outb[seg];                        // out-incidences of v before i
+        const uint32_t ib = (uint32_t)(i - seg) - ob;                   // in-incidences of v before i
+        if ((ent & 1u) == 0) {            // e in OUT(v), v = src(e)
+            const uint32_t pos = off_out[v] + ob;
+            rec[pos] = ((uint64_t)e << 32) | dst[e];
+            rank[e] = pos + 1;                                             // var 0: OUT(src e)
+            rank[m + e] = off_in[v] + ib + (src[e] == dst[e] ? 1u : 0u);  // var 1: IN(src e), ids <= e
+        } else {                          // e in IN(v), v = dst(e)
+            const uint32_t pos = off_in[v] + ib;
+            rec[pos] = ((uint64_t)e << 32) | src[e];
+            rank[3 * m + e] = pos + 1;                                     // var 3: IN(dst e)
+            rank[2 * m + e] = off_out[v] + ob;                             // var 2: OUT(dst e), ids <= e
+        }
     }
 }
 
@@ -83,49 +168,68 @@ cudaError_t dmalloc(T **p, size_t count) { return cudaMalloc((void **)p, std::ma
 
 void free_graph(DeviceGraph &d) {
     cudaFree(d.src); cudaFree(d.dst); cudaFree(d.t); cudaFree(d.perm);
-    cudaFree(d.off_out); cudaFree(d.off_in); cudaFree(d.rec);
+    cudaFree(d.off_out); cudaFree(d.off_in); cudaFree(d.rec); cudaFree(d.rank);
     d = DeviceGraph{};
 }
 
-// one direction of the CSR: sort ids by key vertex (stable, so ids stay
-// ascending = chronological inside each vertex), offsets by histogram + scan
-cudaError_t build_direction(const uint32_t *key, const uint32_t *nbr, uint64_t m, uint32_t n, uint32_t bias,
-                            uint32_t *off, uint64_t *rec, cudaStream_t s) {
-    uint32_t *ids_in = nullptr, *ids_out = nullptr, *keys_out = nullptr, *deg = nullptr;
+// Offsets (histogram + scan per direction), then the merged incidence sort.
+cudaError_t build_csr(DeviceGraph &d, cudaStream_t s) {
+    const uint64_t m = d.m;
+    const uint32_t n = d.n;
+    uint32_t *deg = nullptr, *key = nullptr, *val = nullptr, *kout = nullptr, *vout = nullptr, *flag = nullptr;
     void *tmp = nullptr;
-    size_t tmp_bytes = 0, scan_bytes = 0;
+    size_t sort_bytes = 0, scan_bytes = 0, scan2_bytes = 0;
     cudaError_t err;
     int end_bit = 1;
     while (end_bit < 32 && (1ull << end_bit) < (uint64_t)n) end_bit++;
+    const uint64_t n2 = 2 * m;
 #define TRY(x) do { err = (x); if (err != cudaSuccess) goto done; } while (0)
-    TRY(dmalloc(&ids_in, m));
-    TRY(dmalloc(&ids_out, m));
-    TRY(dmalloc(&keys_out, m));
-    TRY(dmalloc(&deg, (size_t)n + 1));
-    TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, keys_out, ids_in, ids_out, (int64_t)m, 0, end_bit, s));
-    TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, deg, off, (int64_t)n + 1, s));
-    TRY(cudaMalloc(&tmp, std::max(tmp_bytes, scan_bytes)));
+    TRY(dmalloc(&deg, 2 * ((size_t)n + 1)));
+    TRY(dmalloc(&key, n2 + 1));
+    TRY(dmalloc(&val, n2));
+    TRY(dmalloc(&kout, n2));
+    TRY(dmalloc(&vout, n2));
+    TRY(dmalloc(&flag, n2 + 1));
+    TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, key, kout, val, vout, (int64_t)n2, 0, end_bit, s));
+    TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, deg, d.off_out, (int64_t)n + 1, s));
+    TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan2_bytes, flag, key, (int64_t)n2 + 1, s));
+    TRY(cudaMalloc(&tmp, std::max(sort_bytes, std::max(scan_bytes, scan2_bytes))));
+    TRY(cudaMemsetAsync(deg, 0, 2 * ((size_t)n + 1) * 4, s));
     if (m) {
-        k_iota<<<grid_for(m), 256, 0, s>>>(ids_in, m);
-        TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, keys_out, ids_in, ids_out, (int64_t)m, 0, end_bit, s));
+        k_degree<<<grid_for(m), 256, 0, s>>>(d.src, m, deg);
+        k_degree<<<grid_for(m), 256, 0, s>>>(d.dst, m, deg + n + 1);
     }
-    TRY(cudaMemsetAsync(deg, 0, ((size_t)n + 1) * 4, s));
-    if (m) k_degree<<<grid_for(m), 256, 0, s>>>(key, m, deg);
-    TRY(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, deg, off, (int64_t)n + 1, s));
-    if (bias) k_bias<<<grid_for((uint64_t)n + 1), 256, 0, s>>>(off, n + 1, bias);
-    if (m) k_records<<<grid_for(m), 256, 0, s>>>(ids_out, nbr, m, rec);
+    TRY(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, deg, d.off_out, (int64_t)n + 1, s));
+    TRY(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, deg + n + 1, d.off_in, (int64_t)n + 1, s));
+    k_bias<<<grid_for((uint64_t)n + 1), 256, 0, s>>>(d.off_in, n + 1, (uint32_t)m);
+    if (m) {
+        k_incidences<<<grid_for(n2), 256, 0, s>>>(d.src, d.dst, m, key, val);
+        TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, key, kout, val, vout, (int64_t)n2, 0, end_bit, s));
+        k_outflag<<<grid_for(n2), 256, 0, s>>>(vout, n2, flag);
+        TRY(cudaMemsetAsync(flag + n2, 0, 4, s));
+        TRY(cub::DeviceScan::ExclusiveSum(tmp, scan2_bytes, flag, key, (int64_t)n2 + 1, s));  // key: free after the sort
+        k_scatter_csr<<<grid_for(n2), 256, 0, s>>>(kout, vout, key, d.src, d.dst, d.off_out, d.off_in, m, d.rec,
+                                                   d.rank);
+    }
     TRY(cudaGetLastError());
     TRY(cudaStreamSynchronize(s));
 done:
 #undef TRY
-    cudaFree(ids_in); cudaFree(ids_out); cudaFree(keys_out); cudaFree(deg); cudaFree(tmp);
+    cudaFree(deg); cudaFree(key); cudaFree(val); cudaFree(kout); cudaFree(vout); cudaFree(flag); cudaFree(tmp);
     return err;
 }
 
 }  // namespace
 
-cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, cudaStream_t s) {
-    if (d.m) k_horizon<<<grid_for(d.m), 256, 0, s>>>(d.t, d.m, delta, H);
+size_t horizon_scratch_words(uint64_t m) { return 2 * ((m + kHB - 1) / kHB) + 1; }
+
+// H_delta for every edge: two launches (block ends, then the staged search).
+// scratch: horizon_scratch_words(m) u64 of device memory.
+cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, uint64_t *scratch, cudaStream_t s) {
+    if (!d.m) return cudaSuccess;
+    const uint64_t nb = (d.m + kHB - 1) / kHB;
+    k_horizon_ends<<<grid_for(2 * nb), 256, 0, s>>>(d.t, d.m, delta, scratch);
+    k_horizon<<<(unsigned)nb, kHB, 0, s>>>(d.t, d.m, delta, scratch, H);
     return cudaGetLastError();
 }
 
@@ -154,7 +258,8 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     TRY(dmalloc(&d.perm, m));
     TRY(dmalloc(&d.off_out, (size_t)n + 1));
     TRY(dmalloc(&d.off_in, (size_t)n + 1));
-    TRY(dmalloc(&d.rec, 2 * m));
+    TRY(dmalloc(&d.rec, 2 * m + 4));   // +4: gallop_after's 32-byte vector loads
+    TRY(dmalloc(&d.rank, 4 * m));
     TRY(dmalloc(&flags, 3));
     if (on_dev) {
         isrc = const_cast<uint32_t *>(src); idst = const_cast<uint32_t *>(dst); it = const_cast<int64_t *>(t);
@@ -191,8 +296,7 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     }
     if (m) k_gather<<<grid_for(m), 256, 0, s>>>(d.perm, isrc, idst, it, m, d.src, d.dst, d.t);
     TRY(cudaGetLastError());
-    TRY(build_direction(d.src, d.dst, m, n, 0, d.off_out, d.rec, s));
-    TRY(build_direction(d.dst, d.src, m, n, (uint32_t)m, d.off_in, d.rec + m, s));
+    TRY(build_csr(d, s));
     TRY(cudaStreamSynchronize(s));
 #undef TRY
     if (!on_dev) { cudaFree(isrc); cudaFree(idst); cudaFree(it); }

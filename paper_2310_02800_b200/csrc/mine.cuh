@@ -22,6 +22,8 @@
 // every stack within kCap = 64 tasks.
 #pragma once
 
+#include <utility>
+
 #include "tm_internal.cuh"
 
 namespace tmg {
@@ -29,12 +31,24 @@ namespace tmg {
 constexpr int kCap = 64;             // tasks per level per warp
 constexpr int kWarpsPerBlock = 8;
 constexpr int kRootChunk = 128;      // roots claimed per global atomic
+constexpr int kLeafSectors = 2;      // leaf windows scanned inline up to 8 records
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
     return r;
+}
+
+// Compile-time loop: f(std::integral_constant<int, I>) for I = 0..N-1, so
+// that per-index layout decisions are constant expressions (if constexpr).
+template <class F, int... I>
+__device__ __forceinline__ void sfor_impl(F &&f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void sfor(F &&f) {
+    if constexpr (N > 0) sfor_impl(f, std::make_integer_sequence<int, N>{});
 }
 
 // First position p in [b, e) whose record's edge id is > key (e if none):
@@ -52,6 +66,37 @@ __device__ __forceinline__ uint32_t first_after(const uint64_t *__restrict__ rec
     return b;
 }
 
+// Same answer as first_after, for a key whose answer is expected near b
+// (windows are δ-bounded and short): the first round trip fetches the whole
+// aligned 32-byte sector holding b (records 4k..4k+3, two 16-byte loads in
+// flight together), then gallops sector by sector and binary-searches the
+// bracket.  rec is padded by 4 records, so the vector loads never leave the
+// allocation.
+__device__ __forceinline__ uint32_t gallop_after(const uint64_t *__restrict__ rec, uint32_t b, uint32_t e,
+                                                 uint32_t key) {
+    if (b >= e) return b;
+    const uint32_t a = b & ~3u;
+    const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(rec + a);
+    const ulonglong2 x0 = __ldg(v), x1 = __ldg(v + 1);
+    const uint32_t id[4] = {(uint32_t)(x0.x >> 32), (uint32_t)(x0.y >> 32), (uint32_t)(x1.x >> 32),
+                            (uint32_t)(x1.y >> 32)};
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const uint32_t p = a + k;
+        if (p >= b && p < e && id[k] > key) return p;
+    }
+    if (a + 4 >= e) return e;
+    uint32_t lo = a + 4, step = 4, hi;
+    while (true) {
+        hi = lo + step - 1;
+        if (hi >= e) { hi = e; break; }
+        if ((uint32_t)(__ldg(rec + hi) >> 32) > key) break;
+        lo = hi + 1;
+        step <<= 1;
+    }
+    return first_after(rec, lo, hi, key);
+}
+
 __device__ __forceinline__ uint32_t ceil_log2p1(uint32_t len) {  // ceil(log2(len+1))
     return len ? 32 - __clz(len) : 0;
 }
@@ -64,65 +109,168 @@ __device__ __forceinline__ uint64_t warp_sum_u31(uint32_t v) {
 }
 
 // ------------------------------------------------------------------ plans
-// Compile-time plan: the motif structure is a template argument, so every
-// per-level choice (which list, which checks, how many mapped vertices) is a
-// constant — the B200 counterpart of the paper's generated motif-specific
-// code and `minfo`.
-template <uint64_t CODE>
-struct PlanC {
-    static constexpr int kL = (int)(CODE & 7);
-    __host__ __device__ static constexpr int u_(int i) { return (int)((CODE >> (3 + 6 * i)) & 7); }
-    __host__ __device__ static constexpr int v_(int i) { return (int)((CODE >> (6 + 6 * i)) & 7); }
-    __host__ __device__ static constexpr int nv_(int l) {
+// Static decode of a motif, the `minfo` of P:739-780: for motif edge l
+// (0-based) which endpoints are already mapped, which adjacency list supplies
+// the candidates, and which earlier matched edge anchors the window's lower
+// bound.  Used at compile time (PlanC) and at run time (PlanR).
+struct Shape {
+    int L;
+    int u[kMaxL], v[kMaxL];
+    __host__ __device__ constexpr int nv(int l) const {  // vertices mapped by edges [0, l)
         int mx = -1;
         for (int i = 0; i < l; i++) {
-            mx = u_(i) > mx ? u_(i) : mx;
-            mx = v_(i) > mx ? v_(i) : mx;
+            mx = u[i] > mx ? u[i] : mx;
+            mx = v[i] > mx ? v[i] : mx;
         }
         return mx + 1;
     }
+    __host__ __device__ constexpr int last_touch(int l, int x) const {
+        for (int i = l - 1; i >= 0; --i)
+            if (u[i] == x || v[i] == x) return i;
+        return -1;
+    }
+    // candidate list of motif edge l: 0 = OUT(φ(u_l)), 1 = IN(φ(v_l)).  With
+    // both endpoints mapped (reading Q8) take the list whose vertex
+    // was touched most recently: its window start is one rank load away.
+    __host__ __device__ constexpr int ldir(int l) const {
+        const int nb = nv(l);
+        const bool ub = u[l] < nb, vb = v[l] < nb;
+        if (ub && vb) return last_touch(l, u[l]) > last_touch(l, v[l]) ? 0 : 1;
+        return ub ? 0 : 1;
+    }
+    __host__ __device__ constexpr int lx(int l) const { return ldir(l) == 0 ? u[l] : v[l]; }
+    // the latest matched edge touching the list vertex, and the rank variant
+    // (2 * endpoint + dir) locating it in that list
+    __host__ __device__ constexpr int anc(int l) const { return last_touch(l, lx(l)); }
+    __host__ __device__ constexpr int avar(int l) const { return (u[anc(l)] == lx(l) ? 0 : 2) + ldir(l); }
+    // What a task at level l (l matched edges) must carry for the rest of its
+    // subtree — the paper's "number of valid mappings at each level"
+    // taken one step further: only the φ slots later checks or lists read, the
+    // matched ids later window anchors read, and hi only if windows follow.
+    __host__ __device__ constexpr bool keep_phi(int l, int k) const {
+        if (k >= nv(l)) return false;
+        for (int q = l; q < L; ++q) {          // structural check of motif edge q
+            const int nb = nv(q);
+            if (u[q] < nb && v[q] < nb) {
+                if ((ldir(q) == 0 ? v[q] : u[q]) == k) return true;
+            } else if (k < nb) {
+                return true;                    // injectivity compares against every mapped vertex
+            }
+        }
+        for (int q = l + 1; q < L; ++q)         // list vertex of a later window
+            if (lx(q) == k) return true;
+        return false;
+    }
+    __host__ __device__ constexpr bool keep_eh(int l, int k) const {
+        for (int q = l + 1; q < L; ++q)
+            if (k < l && anc(q) == k) return true;
+        return false;
+    }
+    __host__ __device__ constexpr bool keep_hi(int l) const { return l + 1 < L; }
+};
+
+template <uint64_t CODE>
+__host__ __device__ constexpr Shape shape_of() {
+    Shape s{};
+    s.L = (int)(CODE & 7);
+    for (int i = 0; i < kMaxL; i++) {
+        s.u[i] = i < s.L ? (int)((CODE >> (3 + 6 * i)) & 7) : 0;
+        s.v[i] = i < s.L ? (int)((CODE >> (6 + 6 * i)) & 7) : 0;
+    }
+    return s;
+}
+
+// Compile-time plan: the motif structure is a template argument, so every
+// per-level choice (which list, which checks, how many mapped vertices, the
+// anchor) is a constant — the B200 counterpart of the paper's generated
+// motif-specific code.
+template <uint64_t CODE>
+struct PlanC {
+    static constexpr int kL = shape_of<CODE>().L;
     // φ slots stored with a level-l task
-    __host__ __device__ static constexpr int nslots(int l) { return nv_(l); }
+    __host__ __device__ static constexpr int nslots(int l) { return shape_of<CODE>().nv(l); }
+    __host__ __device__ static constexpr bool keep_phi(int l, int k) { return shape_of<CODE>().keep_phi(l, k); }
+    __host__ __device__ static constexpr bool keep_eh(int l, int k) { return shape_of<CODE>().keep_eh(l, k); }
+    __host__ __device__ static constexpr bool keep_hi(int l) { return shape_of<CODE>().keep_hi(l); }
     __device__ explicit PlanC(const MineParams &) {}
-    __device__ __forceinline__ int L() const { return kL; }
-    __device__ __forceinline__ int u(int i) const { return u_(i); }
-    __device__ __forceinline__ int v(int i) const { return v_(i); }
-    __device__ __forceinline__ int nv(int l) const { return nv_(l); }
+    // every accessor is forced through a constant expression, so no decode
+    // survives to run time (no local-memory copy of the Shape)
+    __device__ __forceinline__ static constexpr int L() { return kL; }
+    template <int I> __device__ __forceinline__ static constexpr int u() { constexpr int r = shape_of<CODE>().u[I]; return r; }
+    template <int I> __device__ __forceinline__ static constexpr int v() { constexpr int r = shape_of<CODE>().v[I]; return r; }
+    template <int I> __device__ __forceinline__ static constexpr int nv() { constexpr int r = shape_of<CODE>().nv(I); return r; }
+    template <int I> __device__ __forceinline__ static constexpr int ldir() { constexpr int r = shape_of<CODE>().ldir(I); return r; }
+    template <int I> __device__ __forceinline__ static constexpr int lx() { constexpr int r = shape_of<CODE>().lx(I); return r; }
+    template <int I> __device__ __forceinline__ static constexpr int anc() { constexpr int r = shape_of<CODE>().anc(I); return r; }
+    template <int I> __device__ __forceinline__ static constexpr int avar() { constexpr int r = shape_of<CODE>().avar(I); return r; }
 };
 
 // Runtime plan: the same kernel body for any prefix-connected motif with
-// L <= kMaxL edges, the structure read from the launch parameters.
+// L <= kMaxL edges, the decode computed per thread from the launch
+// parameters.
 struct PlanR {
     static constexpr int kL = kMaxL;
     __host__ __device__ static constexpr int nslots(int l) { return l + 1 < kMaxV ? l + 1 : kMaxV; }
+    __host__ __device__ static constexpr bool keep_phi(int l, int k) { return k < nslots(l); }
+    __host__ __device__ static constexpr bool keep_eh(int, int) { return true; }
+    __host__ __device__ static constexpr bool keep_hi(int) { return true; }
     int L_;
-    int nv__[kMaxL + 1];
-    const MineParams &p_;
-    __device__ explicit PlanR(const MineParams &p) : L_((int)p.L), p_(p) {
-        int mx = -1;
-        nv__[0] = 0;
+    int u_[kMaxL], v_[kMaxL], nv_[kMaxL + 1], ldir_[kMaxL], lx_[kMaxL], anc_[kMaxL], avar_[kMaxL];
+    __device__ explicit PlanR(const MineParams &p) {
+        Shape s{};
+        s.L = (int)p.L;
 #pragma unroll
         for (int i = 0; i < kMaxL; i++) {
-            if (i < L_) {
-                mx = max(mx, (int)p.u[i]);
-                mx = max(mx, (int)p.v[i]);
-            }
-            nv__[i + 1] = mx + 1;
+            s.u[i] = i < s.L ? p.u[i] : 0;
+            s.v[i] = i < s.L ? p.v[i] : 0;
+        }
+        L_ = s.L;
+#pragma unroll
+        for (int i = 0; i <= kMaxL; i++) nv_[i] = s.nv(i);
+#pragma unroll
+        for (int i = 0; i < kMaxL; i++) {
+            u_[i] = s.u[i];
+            v_[i] = s.v[i];
+            const bool live = i >= 1 && i < s.L;
+            ldir_[i] = live ? s.ldir(i) : 0;
+            lx_[i] = live ? s.lx(i) : 0;
+            anc_[i] = live ? s.anc(i) : 0;
+            avar_[i] = live ? s.avar(i) : 0;
         }
     }
     __device__ __forceinline__ int L() const { return L_; }
-    __device__ __forceinline__ int u(int i) const { return p_.u[i]; }
-    __device__ __forceinline__ int v(int i) const { return p_.v[i]; }
-    __device__ __forceinline__ int nv(int l) const { return nv__[l]; }
+    template <int I> __device__ __forceinline__ int u() const { return u_[I]; }
+    template <int I> __device__ __forceinline__ int v() const { return v_[I]; }
+    template <int I> __device__ __forceinline__ int nv() const { return nv_[I]; }
+    template <int I> __device__ __forceinline__ int ldir() const { return ldir_[I]; }
+    template <int I> __device__ __forceinline__ int lx() const { return lx_[I]; }
+    template <int I> __device__ __forceinline__ int anc() const { return anc_[I]; }
+    template <int I> __device__ __forceinline__ int avar() const { return avar_[I]; }
 };
 
 // ------------------------------------------------------- shared-memory layout
 // Per warp, per level l = 1..kL-1, a structure of arrays of kCap tasks:
-//   [0] lo  [1] up  [2] hi  [3 .. 3+S) φ  [.. +l) matched ids (kEnum)  [+1] root slot (kRoots)
+//   [0] lo  [1] up  [2] hi  [3 .. 3+S) φ  [.. +l) matched edge ids  [+1] root slot (kRoots)
 template <class Plan, int MODE>
 struct Layout {
-    __host__ __device__ static constexpr int eh(int l) { return 3 + Plan::nslots(l); }
-    __host__ __device__ static constexpr int rs(int l) { return eh(l) + (MODE == kEnum ? l : 0); }
+    // [0] lo  [1] up  [2 ..) kept φ slots  [hi]  kept matched edge ids  [root slot (kRoots)]
+    __host__ __device__ static constexpr bool kphi(int l, int k) { return MODE == kStats || Plan::keep_phi(l, k); }
+    __host__ __device__ static constexpr bool keh(int l, int k) {
+        return k < l && (MODE == kEnum || MODE == kStats || Plan::keep_eh(l, k));
+    }
+    __host__ __device__ static constexpr bool khi(int l) { return MODE == kStats || Plan::keep_hi(l); }
+    __host__ __device__ static constexpr int phi(int l, int k) {
+        int f = 2;
+        for (int i = 0; i < k; i++) f += kphi(l, i) ? 1 : 0;
+        return f;
+    }
+    __host__ __device__ static constexpr int hi(int l) { return phi(l, Plan::nslots(l)); }
+    __host__ __device__ static constexpr int eh(int l, int k) {
+        int f = hi(l) + (khi(l) ? 1 : 0);
+        for (int i = 0; i < k; i++) f += keh(l, i) ? 1 : 0;
+        return f;
+    }
+    __host__ __device__ static constexpr int rs(int l) { return eh(l, l); }
     __host__ __device__ static constexpr int fields(int l) { return rs(l) + (MODE == kRoots ? 1 : 0); }
     __host__ __device__ static constexpr int off(int l) {  // word offset of level l
         int o = 0;
@@ -143,7 +291,7 @@ __device__ __forceinline__ uint32_t pick(const uint32_t (&a)[N], int k) {
 
 struct Stats {
     unsigned long long nodes[kMaxL];
-    unsigned long long window, list, probes;
+    unsigned long long window, list, probes, fast_window;
 };
 
 template <class Plan, int MODE>
@@ -155,21 +303,57 @@ struct Warp {
     int lane;
     uint32_t ntask[LM + 1];
     uint64_t cand[LM + 1];
-    unsigned long long count;   // lane 0: matches found by this warp
+    unsigned long long count;        // lane 0: matches found by batch expansion
+    unsigned long long leaf_count;   // per lane: matches found by leaf scans
     Stats st;
 
     __device__ Warp(const MineParams &p_, const Plan &pl, uint32_t *w, int ln) : p(p_), plan(pl), ws(w), lane(ln) {
 #pragma unroll
         for (int i = 0; i <= LM; i++) { ntask[i] = 0; cand[i] = 0; }
         count = 0;
+        leaf_count = 0;
         if (MODE == kStats) {
 #pragma unroll
             for (int i = 0; i < kMaxL; i++) st.nodes[i] = 0;
-            st.window = st.list = st.probes = 0;
+            st.window = st.list = st.probes = st.fast_window = 0;
         }
     }
 
-    __device__ __forceinline__ uint32_t *field(int l, int f) { return ws + Layout<Plan, MODE>::off(l) + f * kCap; }
+    // SoA column F of level L_ (both compile-time: the offset is a constant)
+    template <int L_, int F>
+    __device__ __forceinline__ uint32_t *fld() const {
+        constexpr int o = Layout<Plan, MODE>::off(L_) + F * kCap;
+        return ws + o;
+    }
+
+    // StructConstraints of a candidate record for motif edge LV,
+    // with the plan's static checks.  w: the record's neighbour,
+    // from_out: the record comes from the out-list of φ(u_LV) (w is its
+    // destination) rather than the in-list of φ(v_LV) (w is its source).
+    template <int LV, int N>
+    __device__ __forceinline__ bool accept(uint32_t w, bool from_out, const uint32_t (&phi)[N]) const {
+        const int uM = plan.template u<LV>(), vM = plan.template v<LV>(), nb = plan.template nv<LV>();
+        if (uM < nb && vM < nb) return from_out ? (w == pick(phi, vM)) : (w == pick(phi, uM));
+        bool ok = true;  // the new endpoint must be a graph vertex not yet mapped (injectivity)
+#pragma unroll
+        for (int k = 0; k < N; k++)
+            if (k < nb) ok &= (w != phi[k]);
+        return ok;
+    }
+
+    // enumerate one match found by a leaf scan: eh[0..nl-2], e, last
+    template <int NE>
+    __device__ __forceinline__ void emit_one(const uint32_t (&eh)[NE], uint32_t e, uint32_t last, int nl) {
+        const unsigned long long row = atomicAdd(&p.scratch[2], 1ull);
+        if (row < p.cap) {
+            uint32_t *dst = p.enum_buf + row * (uint64_t)(nl + 1);
+#pragma unroll
+            for (int i = 0; i < NE; i++)
+                if (i < nl - 1) dst[i] = eh[i] + p.id_offset;
+            dst[nl - 1] = e + p.id_offset;
+            dst[nl] = last + p.id_offset;
+        }
+    }
 
     // Emit the matches of the lanes with `ok` (last motif edge matched).
     // eh: the L-1 earlier edge ids, e: the last one.
@@ -207,29 +391,88 @@ struct Warp {
                                          const uint32_t (&eh)[NE], uint32_t rslot) {
         uint32_t lo = 0, up = 0;
         if (ok) {
-            const int uM = plan.u(NL), vM = plan.v(NL), nb = plan.nv(NL);
-            const bool ub = uM < nb, vb = vM < nb;
-            const uint32_t xu = pick(phi, uM), xv = pick(phi, vM);
-            uint32_t b, en;
-            if (ub && vb) {  // both endpoints mapped: scan the shorter list (reading Q8)
-                uint32_t ob = __ldg(p.off_out + xu), oe = __ldg(p.off_out + xu + 1);
-                uint32_t ib = __ldg(p.off_in + xv), ie = __ldg(p.off_in + xv + 1);
-                if (oe - ob < ie - ib) { b = ob; en = oe; } else { b = ib; en = ie; }
-            } else if (ub) {
-                b = __ldg(p.off_out + xu); en = __ldg(p.off_out + xu + 1);
-            } else {
-                b = __ldg(p.off_in + xv); en = __ldg(p.off_in + xv + 1);
-            }
-            uint32_t lim = hi;
             const uint32_t *hf = p.Hf[NL - 1];
-            if (hf) lim = min(lim, __ldg(hf + e));
-            lo = first_after(p.rec, b, en, e);
-            up = first_after(p.rec, lo, en, lim);
+            const uint32_t lim = hf ? min(hi, __ldg(hf + e)) : hi;   // min(t_root + δ, t_prev + δ_i) as an id
             if (MODE == kStats) {
+                // instrumentation of Algorithm 1 itself: shorter list (Q8), two binary searches
+                const int uM = plan.template u<NL>(), vM = plan.template v<NL>(), nb = plan.template nv<NL>();
+                const bool ub = uM < nb, vb = vM < nb;
+                const uint32_t xu = pick(phi, uM), xv = pick(phi, vM);
+                uint32_t b, en;
+                if (ub && vb) {
+                    uint32_t ob = __ldg(p.off_out + xu), oe = __ldg(p.off_out + xu + 1);
+                    uint32_t ib = __ldg(p.off_in + xv), ie = __ldg(p.off_in + xv + 1);
+                    if (oe - ob < ie - ib) { b = ob; en = oe; } else { b = ib; en = ie; }
+                } else if (ub) {
+                    b = __ldg(p.off_out + xu); en = __ldg(p.off_out + xu + 1);
+                } else {
+                    b = __ldg(p.off_in + xv); en = __ldg(p.off_in + xv + 1);
+                }
+                lo = first_after(p.rec, b, en, e);
+                up = first_after(p.rec, lo, en, lim);
+                {   // the window the fast path (below) scans for the same node
+                    const int dir = plan.template ldir<NL>();
+                    const uint32_t x = pick(phi, plan.template lx<NL>());
+                    const uint32_t fb = __ldg((dir == 0 ? p.off_out : p.off_in) + x);
+                    const uint32_t fe = __ldg((dir == 0 ? p.off_out : p.off_in) + x + 1);
+                    const uint32_t flo = first_after(p.rec, fb, fe, e);
+                    st.fast_window += first_after(p.rec, flo, fe, lim) - flo;
+                }
                 st.nodes[NL] += 1;
                 st.window += up - lo;
                 st.list += en - b;
                 st.probes += ceil_log2p1(en - b);
+            } else {
+                // window start: one rank load at the anchor edge (the latest
+                // matched edge touching the list vertex), then a short gallop
+                // to "after e_prev" if the anchor is older than e_prev; window
+                // end: gallop from the start (windows are short, δ-bounded)
+                const int dir = plan.template ldir<NL>(), var = plan.template avar<NL>(), j = plan.template anc<NL>();
+                const uint32_t x = pick(phi, plan.template lx<NL>());
+                const uint32_t ea = (j == NL - 1) ? e : pick(eh, j);
+                const uint32_t en = __ldg((dir == 0 ? p.off_out : p.off_in) + x + 1);
+                lo = __ldg(p.rank + (size_t)var * p.m + ea);
+                if (j != NL - 1) lo = gallop_after(p.rec, lo, en, e);
+                if (NL + 1 == plan.L()) {
+                    // leaf parent: the last motif edge's window is scanned in
+                    // this lane, sector by sector, and its matches counted
+                    // (or emitted) on the spot; only a window longer than
+                    // kLeafSectors sectors leaves a remainder task for the
+                    // warp-cooperative path
+                    uint32_t pp = lo;
+                    bool done = false;
+                    uint32_t cnt = 0;
+#pragma unroll 1
+                    for (int it = 0; it < kLeafSectors && !done; ++it) {
+                        const uint32_t a = pp & ~3u;
+                        const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(p.rec + a);
+                        const ulonglong2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
+                        const uint64_t r4[4] = {x0.x, x0.y, x1.x, x1.y};
+#pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            const uint32_t q = a + k;
+                            if (done || q < pp) continue;
+                            const uint32_t id = (uint32_t)(r4[k] >> 32), w = (uint32_t)r4[k];
+                            if (q >= en || id > lim) { done = true; continue; }
+                            if (accept<NL>(w, dir == 0, phi)) {
+                                cnt++;
+                                if (MODE == kEnum) emit_one<NE>(eh, e, id, NL);
+                            }
+                        }
+                        pp = a + 4;
+                        if (pp >= en) done = true;
+                    }
+                    leaf_count += cnt;
+                    if (MODE == kRoots && cnt) atomicAdd(&p.root_counts[rslot], (unsigned long long)cnt);
+                    if (done) {
+                        lo = up = 0;
+                    } else {
+                        lo = pp;
+                        up = gallop_after(p.rec, pp, en, lim);
+                    }
+                } else {
+                    up = gallop_after(p.rec, lo, en, lim);
+                }
             }
         }
         const bool keep = ok && up > lo;
@@ -237,17 +480,20 @@ struct Warp {
         if (!mask) return;
         if (keep) {
             const uint32_t slot = ntask[NL] + __popc(mask & lanemask_lt());
-            field(NL, 0)[slot] = lo;
-            field(NL, 1)[slot] = up;
-            field(NL, 2)[slot] = hi;
+            using Lay = Layout<Plan, MODE>;
+            fld<NL, 0>()[slot] = lo;
+            fld<NL, 1>()[slot] = up;
             constexpr int S = Plan::nslots(NL);
-#pragma unroll
-            for (int k = 0; k < S; k++) field(NL, 3 + k)[slot] = phi[k < NS ? k : 0];
-            if (MODE == kEnum) {
-#pragma unroll
-                for (int k = 0; k < NL; k++) field(NL, Layout<Plan, MODE>::eh(NL) + k)[slot] = (k < NL - 1) ? eh[k < NE ? k : 0] : e;
-            }
-            if (MODE == kRoots) field(NL, Layout<Plan, MODE>::rs(NL))[slot] = rslot;
+            sfor<S>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                if constexpr (Lay::kphi(NL, k)) fld<NL, Lay::phi(NL, k)>()[slot] = phi[k < NS ? k : 0];
+            });
+            if constexpr (Lay::khi(NL)) fld<NL, Lay::hi(NL)>()[slot] = hi;
+            sfor<NL>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                if constexpr (Lay::keh(NL, k)) fld<NL, Lay::eh(NL, k)>()[slot] = (k < NL - 1) ? eh[k < NE ? k : 0] : e;
+            });
+            if constexpr (MODE == kRoots) fld<NL, Lay::rs(NL)>()[slot] = rslot;
         }
         ntask[NL] += __popc(mask);
         cand[NL] += warp_sum_u31(keep ? up - lo : 0u);
@@ -290,8 +536,9 @@ struct Warp {
     template <int LV>
     __device__ __forceinline__ void expand() {
         constexpr int S = Plan::nslots(LV);
+        using Lay = Layout<Plan, MODE>;
         const uint32_t n = ntask[LV];
-        uint32_t *flo = field(LV, 0), *fup = field(LV, 1);
+        uint32_t *flo = fld<LV, 0>(), *fup = fld<LV, 1>();
         const int j = (int)n - 1 - lane;               // lane i looks at the i-th task from the top
         uint32_t lo = 0, sz = 0;
         if (j >= 0) { lo = flo[j]; sz = fup[j] - lo; }
@@ -321,29 +568,22 @@ struct Warp {
         uint32_t hi = 0, rslot = 0, e = 0, w = 0;
         bool ok = false;
         if (active) {
-#pragma unroll
-            for (int k = 0; k < S; k++) phi[k] = field(LV, 3 + k)[jt];
-            hi = field(LV, 2)[jt];
-            if (MODE == kEnum) {
-#pragma unroll
-                for (int k = 0; k < LV; k++) eh[k] = field(LV, Layout<Plan, MODE>::eh(LV) + k)[jt];
-            }
-            if (MODE == kRoots) rslot = field(LV, Layout<Plan, MODE>::rs(LV))[jt];
+            sfor<S>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                if constexpr (Lay::kphi(LV, k)) phi[k] = fld<LV, Lay::phi(LV, k)>()[jt];
+                else phi[k] = 0u;
+            });
+            if constexpr (Lay::khi(LV)) hi = fld<LV, Lay::hi(LV)>()[jt];
+            sfor<LV>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                if constexpr (Lay::keh(LV, k)) eh[k] = fld<LV, Lay::eh(LV, k)>()[jt];
+                else eh[k] = 0u;
+            });
+            if constexpr (MODE == kRoots) rslot = fld<LV, Lay::rs(LV)>()[jt];
             const uint64_t rc = __ldg(p.rec + pos);
             e = (uint32_t)(rc >> 32);
             w = (uint32_t)rc;
-            // StructConstraints with the plan's static checks
-            const int uM = plan.u(LV), vM = plan.v(LV), nb = plan.nv(LV);
-            const bool ub = uM < nb, vb = vM < nb;
-            if (ub && vb) {
-                // record from the out-list of φ(u): w is the destination; from the in-list of φ(v): the source
-                ok = (pos < p.m) ? (w == pick(phi, vM)) : (w == pick(phi, uM));
-            } else {
-                ok = true;  // the new endpoint must be a graph vertex not yet mapped (injectivity)
-#pragma unroll
-                for (int k = 0; k < S; k++)
-                    if (k < nb) ok &= (w != phi[k]);
-            }
+            ok = accept<LV>(w, pos < p.m, phi);
         }
         __syncwarp();
         // consume: pop the fully taken tasks, advance the partially taken one
@@ -355,13 +595,13 @@ struct Warp {
         if (LV + 1 == plan.L()) {
             emit(ok, eh, e, rslot);
         } else if constexpr (LV + 1 < LM) {
-            const int nb = plan.nv(LV);
+            const int nb = plan.template nv<LV>();
             constexpr int S2 = Plan::nslots(LV + 1);
             uint32_t phi2[S2 + 1];
 #pragma unroll
             for (int k = 0; k < S2; k++) phi2[k] = (k < S) ? phi[k < S ? k : 0] : 0u;
             // a new endpoint gets the next slot (motif vertices are numbered by first appearance)
-            if (nb < plan.nv(LV + 1)) {
+            if (nb < plan.template nv<LV + 1>()) {
 #pragma unroll
                 for (int k = 0; k < S2; k++)
                     if (k == nb) phi2[k] = w;
@@ -371,8 +611,11 @@ struct Warp {
     }
 };
 
+#ifndef TM_MIN_BLOCKS
+#define TM_MIN_BLOCKS 1
+#endif
 template <class Plan, int MODE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) mine_kernel(const MineParams p) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, TM_MIN_BLOCKS) mine_kernel(const MineParams p) {
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int LM = Plan::kL;
@@ -409,7 +652,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) mine_kernel(const MinePar
             default: break;
         }
     }
-    if (lane == 0 && W.count) atomicAdd(&p.scratch[1], W.count);
+    unsigned long long tot = W.leaf_count;
+    for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(kFull, tot, d);
+    tot += W.count;   // lane 0's batch count (other lanes hold 0)
+    if (lane == 0 && tot) atomicAdd(&p.scratch[1], tot);
     if (MODE == kStats) {
 #pragma unroll
         for (int l = 0; l < kMaxL; l++) {
@@ -417,16 +663,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) mine_kernel(const MinePar
             for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
             if (lane == 0 && v) atomicAdd(&p.scratch[kStatsBase + l], v);
         }
-        unsigned long long a = W.st.window, b = W.st.list, c = W.st.probes;
+        unsigned long long a = W.st.window, b = W.st.list, c = W.st.probes, f = W.st.fast_window;
         for (int d = 16; d; d >>= 1) {
             a += __shfl_xor_sync(kFull, a, d);
             b += __shfl_xor_sync(kFull, b, d);
             c += __shfl_xor_sync(kFull, c, d);
+            f += __shfl_xor_sync(kFull, f, d);
         }
         if (lane == 0) {
             atomicAdd(&p.scratch[16], a);
             atomicAdd(&p.scratch[17], b);
             atomicAdd(&p.scratch[18], c);
+            atomicAdd(&p.scratch[19], f);
         }
     }
 }

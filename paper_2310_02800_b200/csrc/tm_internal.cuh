@@ -22,6 +22,11 @@ constexpr int kMaxV = TM_MAX_VERTICES;   // motif vertices
 //   off_out   : n+1 offsets into rec (values in [0, m]).
 //   off_in    : n+1 offsets into rec, pre-biased by m (values in [m, 2m]).
 //   perm      : perm[id] = input position.
+//   rank      : 4m u32, rank[var*m + e] = absolute position in rec of the first
+//               record after edge e in one list touching e, var = 2*endpoint
+//               + dir: 0 OUT(src e) (own), 1 IN(src e), 2 OUT(dst e),
+//               3 IN(dst e) (own).  Turns the lower-bound binary search of
+//               GetCandidateEdgeList into one load.
 struct DeviceGraph {
     uint64_t m = 0;
     uint32_t n = 0;
@@ -30,6 +35,7 @@ struct DeviceGraph {
     uint32_t *perm = nullptr;
     uint32_t *off_out = nullptr, *off_in = nullptr;
     uint64_t *rec = nullptr;
+    uint32_t *rank = nullptr;
 };
 
 }  // namespace tmg
@@ -66,6 +72,7 @@ struct MineParams {
     const uint32_t *src, *dst;
     const uint32_t *off_out, *off_in;
     const uint64_t *rec;
+    const uint32_t *rank;              // DeviceGraph::rank
     uint32_t m;
     const uint32_t *H;                 // H_δ  (coarse δ-horizon)
     const uint32_t *Hf[kMaxL];         // H_{δ_i} per gap i, nullptr when δ_i = ∞
@@ -82,7 +89,7 @@ struct MineParams {
 };
 
 constexpr int kScratchWords = 32;
-constexpr int kStatsBase = 8;   // scratch[8 + l] nodes[l], [16] window, [17] list, [18] probes
+constexpr int kStatsBase = 8;   // scratch[8 + l] nodes[l], [16] window, [17] list, [18] probes, [19] fast window
 
 using MineKernel = void (*)(MineParams);
 

@@ -16,7 +16,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtmotif.so")
+# TMOTIF_LIB selects a tuning variant of the same library (variants/<name>/libtmotif.so)
+LIB_PATH = os.environ.get("TMOTIF_LIB") or os.path.join(_HERE, "libtmotif.so")
 
 TM_OK, TM_EINVAL, TM_ENOMEM, TM_ECUDA, TM_EUNSUPPORTED, TM_TRUNCATED = range(6)
 DELTA_INF = (1 << 63) - 1
@@ -45,7 +46,7 @@ class RunOpts(ctypes.Structure):
 
 class SearchStats(ctypes.Structure):
     _fields_ = [("nodes", _u64 * 8), ("window_sum", _u64), ("list_sum", _u64), ("probe_sum", _u64),
-                ("matches", _u64)]
+                ("matches", _u64), ("fast_window_sum", _u64)]
 
 
 class RunInfo(ctypes.Structure):
@@ -273,7 +274,7 @@ def tm_search_stats_run(g: Graph, mo: Motif, **opts) -> dict:
     o = run_opts(**opts)
     _check(lib().tm_search_stats_run(g.handle, mo.handle, ctypes.byref(o), ctypes.byref(s)))
     return {"nodes": list(s.nodes), "window_sum": s.window_sum, "list_sum": s.list_sum,
-            "probe_sum": s.probe_sum, "matches": s.matches}
+            "probe_sum": s.probe_sum, "matches": s.matches, "fast_window_sum": s.fast_window_sum}
 
 
 def tm_last_run_info() -> dict:

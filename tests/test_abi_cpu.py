@@ -90,4 +90,4 @@ def test_partition_plan_tiles_roots_and_covers_halo():
 def test_declared_struct_sizes_match_binding():
     # the ctypes mirrors must match the C layout (x86-64 SysV)
     assert ctypes.sizeof(T.RunOpts) == 8 + 8 * 3 + 4 * 2 + 4 * 2
-    assert ctypes.sizeof(T.SearchStats) == 8 * 12
+    assert ctypes.sizeof(T.SearchStats) == 8 * 13

@@ -283,3 +283,17 @@ def test_generic_and_specialised_kernels_agree():
         mo = T.Motif(mot, 3600)
         assert mo.specialised
         assert T.tm_count(g, mo) == int(T.tm_count_roots(g, mo, allr).sum())  # roots mode = generic kernel
+
+
+def test_bursts_and_equal_timestamps():
+    """Long runs of equal timestamps (horizon blocks whose answer range
+    overflows the shared-memory stage) and sparse stretches."""
+    rng = np.random.default_rng(21)
+    m, n = 12000, 30
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    t = np.concatenate([np.full(5000, 100), np.sort(rng.integers(101, 100000, 2000)), np.full(5000, 200000)])
+    t = t.astype(np.int64)
+    for motif, delta, fine in ((M.TRI, 0, None), (M.PATH2, 50, None), (M.C4, 500, [0, 100, 100]),
+                               (M.STAR3, 1000, None)):
+        check_case(src, dst, t, n, motif, delta, fine, rows=False, roots=False)
