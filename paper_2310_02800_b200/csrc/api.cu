@@ -2,6 +2,7 @@
 // canonicalisation, the per-query horizon construction and the mining
 // launch.  Every step of the hot path runs in this library's kernels.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -107,6 +108,7 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     std::memset(&p, 0, sizeof p);
     p.src = d.src; p.dst = d.dst; p.off_out = d.off_out; p.off_in = d.off_in; p.rec = d.rec; p.rank = d.rank;
     p.m = (uint32_t)m;
+    p.split = (uint32_t)(m + d.n);
     p.L = mo->L;
     for (uint32_t i = 0; i < mo->L; i++) { p.u[i] = mo->u[i]; p.v[i] = mo->v[i]; }
     if (roots_dev) {
@@ -211,6 +213,14 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     cudaEventElapsedTime(&g_info.mine_ms, ev[1], ev[2]);
     cudaEventElapsedTime(&g_info.total_ms, ev[0], ev[3]);
     out->count = mode == kEnum ? host[2] : host[1];
+#ifdef TM_PHASE_PROFILE
+    fprintf(stderr, "[phase]");
+    for (int l = 0; l < 6; l++)
+        if (host[21 + 2 * l])
+            fprintf(stderr, " L%d: steps=%llu cyc/step=%.0f share=%.3f", l, host[21 + 2 * l],
+                    (double)host[20 + 2 * l] / host[21 + 2 * l], 0.0 + host[20 + 2 * l]);
+    fprintf(stderr, "\n");
+#endif
     for (int i = 0; i < kScratchWords; i++) out->stats[i] = host[i];
     return TM_OK;
 }
@@ -220,6 +230,7 @@ tm_status check_graph_args(const uint32_t *src, const uint32_t *dst, const int64
     if (!out) return fail(TM_EINVAL, "out is null");
     *out = nullptr;
     if (m > TM_MAX_M) return fail(TM_EINVAL, "m exceeds TM_MAX_M (2^31-1)");
+    if (m + (uint64_t)n > (1ull << 31) - 4) return fail(TM_EINVAL, "m + n_vertices must stay below 2^31 - 4");
     if (m && (!src || !dst || !t)) return fail(TM_EINVAL, "null edge array");
     if (m && n == 0) return fail(TM_EINVAL, "n_vertices is 0 but m > 0");
     return TM_OK;

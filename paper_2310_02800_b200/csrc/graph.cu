@@ -136,25 +136,44 @@ __global__ void k_outflag(const uint32_t *val, uint64_t n2, uint32_t *flag) {
         flag[i] = (val[i] & 1u) ? 0u : 1u;
 }
 
+// off_out / off_in hold the sentinel-adjusted list starts (plain offset + v,
+// in-lists further shifted by m + n); the plain offsets are recovered here.
 __global__ void k_scatter_csr(const uint32_t *key, const uint32_t *val, const uint32_t *outb, const uint32_t *src,
                               const uint32_t *dst, const uint32_t *off_out, const uint32_t *off_in, uint64_t m,
-                              uint64_t *rec, uint32_t *rank) {
+                              uint32_t n, uint64_t *rec, uint32_t *rank) {
+    const uint32_t split = (uint32_t)(m + n);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 2 * m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = key[i], ent = val[i], e = ent >> 1;
-        const uint64_t seg = (uint64_t)off_out[v] + (off_in[v] - m);   // first incidence of v
+        const uint32_t so = off_out[v], si = off_in[v];                 // list starts in rec
+        const uint64_t seg = (uint64_t)(so - v) + (si - split - v);      // first incidence of v
         const uint32_t ob = outb[i] - outb[seg];                        // out-incidences of v before i
         const uint32_t ib = (uint32_t)(i - seg) - ob;                   // in-incidences of v before i
         if ((ent & 1u) == 0) {            // e in OUT(v), v = src(e)
-            const uint32_t pos = off_out[v] + ob;
+            const uint32_t pos = so + ob;
             rec[pos] = ((uint64_t)e << 32) | dst[e];
-            rank[e] = pos + 1;                                             // var 0: OUT(src e)
-            rank[m + e] = off_in[v] + ib + (src[e] == dst[e] ? 1u : 0u);  // var 1: IN(src e), ids <= e
+            rank[e] = pos + 1;                                       // var 0: OUT(src e)
+            rank[m + e] = si + ib + (src[e] == dst[e] ? 1u : 0u);  // var 1: IN(src e), ids <= e
         } else {                          // e in IN(v), v = dst(e)
-            const uint32_t pos = off_in[v] + ib;
+            const uint32_t pos = si + ib;
             rec[pos] = ((uint64_t)e << 32) | src[e];
-            rank[3 * m + e] = pos + 1;                                     // var 3: IN(dst e)
-            rank[2 * m + e] = off_out[v] + ob;                             // var 2: OUT(dst e), ids <= e
+            rank[3 * m + e] = pos + 1;                               // var 3: IN(dst e)
+            rank[2 * m + e] = so + ob;                               // var 2: OUT(dst e), ids <= e
         }
+    }
+}
+
+// plain exclusive-scan offsets -> sentinel-adjusted list starts
+__global__ void k_adjust_offsets(uint32_t *off_out, uint32_t *off_in, uint32_t n, uint64_t m) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x) {
+        off_out[v] += v;
+        off_in[v] += (uint32_t)(m + n) + v;
+    }
+}
+
+__global__ void k_sentinels(const uint32_t *off_out, const uint32_t *off_in, uint32_t n, uint64_t *rec) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        rec[off_out[v + 1] - 1] = ~0ull;
+        rec[off_in[v + 1] - 1] = ~0ull;
     }
 }
 
@@ -201,15 +220,16 @@ cudaError_t build_csr(DeviceGraph &d, cudaStream_t s) {
     }
     TRY(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, deg, d.off_out, (int64_t)n + 1, s));
     TRY(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, deg + n + 1, d.off_in, (int64_t)n + 1, s));
-    k_bias<<<grid_for((uint64_t)n + 1), 256, 0, s>>>(d.off_in, n + 1, (uint32_t)m);
+    k_adjust_offsets<<<grid_for((uint64_t)n + 1), 256, 0, s>>>(d.off_out, d.off_in, n, m);
+    k_sentinels<<<grid_for(n), 256, 0, s>>>(d.off_out, d.off_in, n, d.rec);
     if (m) {
         k_incidences<<<grid_for(n2), 256, 0, s>>>(d.src, d.dst, m, key, val);
         TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, key, kout, val, vout, (int64_t)n2, 0, end_bit, s));
         k_outflag<<<grid_for(n2), 256, 0, s>>>(vout, n2, flag);
         TRY(cudaMemsetAsync(flag + n2, 0, 4, s));
         TRY(cub::DeviceScan::ExclusiveSum(tmp, scan2_bytes, flag, key, (int64_t)n2 + 1, s));  // key: free after the sort
-        k_scatter_csr<<<grid_for(n2), 256, 0, s>>>(kout, vout, key, d.src, d.dst, d.off_out, d.off_in, m, d.rec,
-                                                   d.rank);
+        k_scatter_csr<<<grid_for(n2), 256, 0, s>>>(kout, vout, key, d.src, d.dst, d.off_out, d.off_in, m, n,
+                                                   d.rec, d.rank);
     }
     TRY(cudaGetLastError());
     TRY(cudaStreamSynchronize(s));
@@ -258,7 +278,8 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     TRY(dmalloc(&d.perm, m));
     TRY(dmalloc(&d.off_out, (size_t)n + 1));
     TRY(dmalloc(&d.off_in, (size_t)n + 1));
-    TRY(dmalloc(&d.rec, 2 * m + 4));   // +4: gallop_after's 32-byte vector loads
+    TRY(dmalloc(&d.rec, 2 * (m + n) + 32));   // sentinels + padding: warp reads may run 31 records past a sentinel
+    TRY(cudaMemsetAsync(d.rec, 0xff, (2 * (m + n) + 32) * sizeof(uint64_t), s));
     TRY(dmalloc(&d.rank, 4 * m));
     TRY(dmalloc(&flags, 3));
     if (on_dev) {

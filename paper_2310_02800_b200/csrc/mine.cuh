@@ -97,6 +97,24 @@ __device__ __forceinline__ uint32_t gallop_after(const uint64_t *__restrict__ re
     return first_after(rec, lo, hi, key);
 }
 
+// First position p >= b with id > key in a sentinel-terminated list (every
+// list ends with an id-0xFFFFFFFF record, so no list end is needed): scans
+// aligned 32-byte sectors, two 16-byte loads each.  Used where the answer is
+// close to b (the lower bound after an older anchor edge).
+__device__ __forceinline__ uint32_t scan_after(const uint64_t *__restrict__ rec, uint32_t b, uint32_t key) {
+    uint32_t a = b & ~3u;
+    while (true) {
+        const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(rec + a);
+        const ulonglong2 x0 = __ldg(v), x1 = __ldg(v + 1);
+        const uint32_t id[4] = {(uint32_t)(x0.x >> 32), (uint32_t)(x0.y >> 32), (uint32_t)(x1.x >> 32),
+                                (uint32_t)(x1.y >> 32)};
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if (a + k >= b && id[k] > key) return a + k;
+        a += 4;
+    }
+}
+
 __device__ __forceinline__ uint32_t ceil_log2p1(uint32_t len) {  // ceil(log2(len+1))
     return len ? 32 - __clz(len) : 0;
 }
@@ -398,15 +416,15 @@ struct Warp {
                 const int uM = plan.template u<NL>(), vM = plan.template v<NL>(), nb = plan.template nv<NL>();
                 const bool ub = uM < nb, vb = vM < nb;
                 const uint32_t xu = pick(phi, uM), xv = pick(phi, vM);
-                uint32_t b, en;
+                uint32_t b, en;   // list [b, en); the sentinel sits at en
                 if (ub && vb) {
-                    uint32_t ob = __ldg(p.off_out + xu), oe = __ldg(p.off_out + xu + 1);
-                    uint32_t ib = __ldg(p.off_in + xv), ie = __ldg(p.off_in + xv + 1);
+                    uint32_t ob = __ldg(p.off_out + xu), oe = __ldg(p.off_out + xu + 1) - 1;
+                    uint32_t ib = __ldg(p.off_in + xv), ie = __ldg(p.off_in + xv + 1) - 1;
                     if (oe - ob < ie - ib) { b = ob; en = oe; } else { b = ib; en = ie; }
                 } else if (ub) {
-                    b = __ldg(p.off_out + xu); en = __ldg(p.off_out + xu + 1);
+                    b = __ldg(p.off_out + xu); en = __ldg(p.off_out + xu + 1) - 1;
                 } else {
-                    b = __ldg(p.off_in + xv); en = __ldg(p.off_in + xv + 1);
+                    b = __ldg(p.off_in + xv); en = __ldg(p.off_in + xv + 1) - 1;
                 }
                 lo = first_after(p.rec, b, en, e);
                 up = first_after(p.rec, lo, en, lim);
@@ -414,7 +432,7 @@ struct Warp {
                     const int dir = plan.template ldir<NL>();
                     const uint32_t x = pick(phi, plan.template lx<NL>());
                     const uint32_t fb = __ldg((dir == 0 ? p.off_out : p.off_in) + x);
-                    const uint32_t fe = __ldg((dir == 0 ? p.off_out : p.off_in) + x + 1);
+                    const uint32_t fe = __ldg((dir == 0 ? p.off_out : p.off_in) + x + 1) - 1;
                     const uint32_t flo = first_after(p.rec, fb, fe, e);
                     st.fast_window += first_after(p.rec, flo, fe, lim) - flo;
                 }
@@ -424,54 +442,57 @@ struct Warp {
                 st.probes += ceil_log2p1(en - b);
             } else {
                 // window start: one rank load at the anchor edge (the latest
-                // matched edge touching the list vertex), then a short gallop
-                // to "after e_prev" if the anchor is older than e_prev; window
-                // end: gallop from the start (windows are short, δ-bounded)
+                // matched edge touching the list vertex), then a short sector
+                // scan to "after e_prev" when the anchor is older than e_prev.
+                // Window end: never searched.  The first sector at lo is read;
+                // if the window ends inside it the task is exact [lo, up),
+                // otherwise it is pushed open-ended (kOpen | lim) and the warp
+                // finds the end while scanning it 32 records at a time.
                 const int dir = plan.template ldir<NL>(), var = plan.template avar<NL>(), j = plan.template anc<NL>();
-                const uint32_t x = pick(phi, plan.template lx<NL>());
                 const uint32_t ea = (j == NL - 1) ? e : pick(eh, j);
-                const uint32_t en = __ldg((dir == 0 ? p.off_out : p.off_in) + x + 1);
                 lo = __ldg(p.rank + (size_t)var * p.m + ea);
-                if (j != NL - 1) lo = gallop_after(p.rec, lo, en, e);
-                if (NL + 1 == plan.L()) {
-                    // leaf parent: the last motif edge's window is scanned in
-                    // this lane, sector by sector, and its matches counted
-                    // (or emitted) on the spot; only a window longer than
-                    // kLeafSectors sectors leaves a remainder task for the
-                    // warp-cooperative path
-                    uint32_t pp = lo;
-                    bool done = false;
-                    uint32_t cnt = 0;
+                if (j != NL - 1) lo = scan_after(p.rec, lo, e);
+                uint32_t pp = lo;
+                bool done = false;
+                uint32_t cnt = 0;
+                const bool leaf = NL + 1 == plan.L();
+                // leaf parent: the last motif edge's window is scanned in this
+                // lane and its matches counted (or emitted) on the spot, for up
+                // to kLeafSectors sectors; non-leaf: one sector to size the window
+                const int nsec = leaf ? kLeafSectors : 1;
 #pragma unroll 1
-                    for (int it = 0; it < kLeafSectors && !done; ++it) {
-                        const uint32_t a = pp & ~3u;
-                        const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(p.rec + a);
-                        const ulonglong2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
-                        const uint64_t r4[4] = {x0.x, x0.y, x1.x, x1.y};
+                for (int it = 0; it < nsec && !done; ++it) {
+                    const uint32_t a4 = pp & ~3u;
+                    const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(p.rec + a4);
+                    const ulonglong2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
+                    const uint64_t r4[4] = {x0.x, x0.y, x1.x, x1.y};
 #pragma unroll
-                        for (int k = 0; k < 4; k++) {
-                            const uint32_t q = a + k;
-                            if (done || q < pp) continue;
-                            const uint32_t id = (uint32_t)(r4[k] >> 32), w = (uint32_t)r4[k];
-                            if (q >= en || id > lim) { done = true; continue; }
-                            if (accept<NL>(w, dir == 0, phi)) {
-                                cnt++;
-                                if (MODE == kEnum) emit_one<NE>(eh, e, id, NL);
-                            }
+                    for (int k = 0; k < 4; k++) {
+                        const uint32_t q = a4 + k;
+                        if (done || q < pp) continue;
+                        const uint32_t id = (uint32_t)(r4[k] >> 32);
+                        if (id > lim) { done = true; up = q; continue; }
+                        if (leaf && accept<NL>((uint32_t)r4[k], dir == 0, phi)) {
+                            cnt++;
+                            if (MODE == kEnum) emit_one<NE>(eh, e, id, NL);
                         }
-                        pp = a + 4;
-                        if (pp >= en) done = true;
                     }
+                    if (!done) pp = a4 + 4;
+                }
+                if (leaf) {
                     leaf_count += cnt;
                     if (MODE == kRoots && cnt) atomicAdd(&p.root_counts[rslot], (unsigned long long)cnt);
-                    if (done) {
-                        lo = up = 0;
-                    } else {
-                        lo = pp;
-                        up = gallop_after(p.rec, pp, en, lim);
-                    }
-                } else {
-                    up = gallop_after(p.rec, lo, en, lim);
+                }
+                if (leaf && done) {
+                    lo = up = 0;                            // fully scanned
+                } else if (!done) {
+                    // exact end: gallop from the first unread sector, bounded by the list's
+                    // sentinel (an open-ended task scanned by the warp measured slower:
+                    // it cannot share a batch with other tasks)
+                    lo = leaf ? pp : lo;                    // a leaf keeps only its unscanned remainder
+                    const uint32_t x = pick(phi, plan.template lx<NL>());
+                    const uint32_t en = __ldg((dir == 0 ? p.off_out : p.off_in) + x + 1) - 1;
+                    up = gallop_after(p.rec, pp, en, lim);
                 }
             }
         }
@@ -583,7 +604,7 @@ struct Warp {
             const uint64_t rc = __ldg(p.rec + pos);
             e = (uint32_t)(rc >> 32);
             w = (uint32_t)rc;
-            ok = accept<LV>(w, pos < p.m, phi);
+            ok = accept<LV>(w, pos < p.split, phi);
         }
         __syncwarp();
         // consume: pop the fully taken tasks, advance the partially taken one
@@ -642,6 +663,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TM_MIN_BLOCKS) mine_kerne
             }
         }
         if (sel < 0) break;
+#ifdef TM_PHASE_PROFILE
+        const long long t0 = clock64();
+#endif
         switch (sel) {
             case 0: roots_left = W.fetch_roots(next, end); break;
             case 1: if constexpr (LM > 1) W.template expand<1>(); break;
@@ -651,6 +675,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TM_MIN_BLOCKS) mine_kerne
             case 5: if constexpr (LM > 5) W.template expand<5>(); break;
             default: break;
         }
+#ifdef TM_PHASE_PROFILE
+        // cycles and steps per selected level (0 = root fetch), scratch[20 + 2*sel]
+        if (lane == 0) {
+            atomicAdd(&p.scratch[20 + 2 * sel], (unsigned long long)(clock64() - t0));
+            atomicAdd(&p.scratch[21 + 2 * sel], 1ull);
+        }
+#endif
     }
     unsigned long long tot = W.leaf_count;
     for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(kFull, tot, d);

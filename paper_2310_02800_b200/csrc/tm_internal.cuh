@@ -15,12 +15,16 @@ constexpr int kMaxV = TM_MAX_VERTICES;   // motif vertices
 // Device-resident temporal graph.
 //   src/dst/t : the chronologically sorted temporal edge list; edge
 //               id = rank by (t, input position) (reading Q1).
-//   rec       : 2m packed 64-bit records (edge id << 32 | neighbour):
-//               [0, m) out-adjacency grouped by source, [m, 2m) in-adjacency
-//               grouped by destination; ascending edge id inside each group
-//               = time order.
-//   off_out   : n+1 offsets into rec (values in [0, m]).
-//   off_in    : n+1 offsets into rec, pre-biased by m (values in [m, 2m]).
+//   rec       : 2(m+n)+32 packed 64-bit records (edge id << 32 | neighbour):
+//               [0, m+n) out-adjacency grouped by source, [m+n, 2(m+n)) in-
+//               adjacency grouped by destination; ascending edge id inside each
+//               group = time order; every group is followed by a
+//               sentinel record 0xFFFFFFFF'FFFFFFFF (id above every bound), so
+//               scans stop by id alone; +32 records of padding (a warp's 32 consecutive
+//               reads of an open window may run past the last sentinel).
+//   off_out   : n+1 start positions in rec (list v = [off_out[v], off_out[v+1]-1),
+//               its sentinel at off_out[v+1]-1).
+//   off_in    : the same for the in-lists (values in [m+n, 2(m+n)]).
 //   perm      : perm[id] = input position.
 //   rank      : 4m u32, rank[var*m + e] = absolute position in rec of the first
 //               record after edge e in one list touching e, var = 2*endpoint
@@ -74,6 +78,7 @@ struct MineParams {
     const uint64_t *rec;
     const uint32_t *rank;              // DeviceGraph::rank
     uint32_t m;
+    uint32_t split;                    // rec positions < split are out-records (m + n)
     const uint32_t *H;                 // H_δ  (coarse δ-horizon)
     const uint32_t *Hf[kMaxL];         // H_{δ_i} per gap i, nullptr when δ_i = ∞
     uint64_t root_lo, n_roots;         // roots root_lo + [0, n_roots) ...
@@ -88,7 +93,7 @@ struct MineParams {
     uint8_t u[kMaxL], v[kMaxL];
 };
 
-constexpr int kScratchWords = 32;
+constexpr int kScratchWords = 40;
 constexpr int kStatsBase = 8;   // scratch[8 + l] nodes[l], [16] window, [17] list, [18] probes, [19] fast window
 
 using MineKernel = void (*)(MineParams);

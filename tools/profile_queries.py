@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default=bench.CONFIG)
 ap.add_argument("--motifs", default=",".join(bench.MOTIFS))
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--grid", type=int, default=0, help="grid_ctas override")
 a = ap.parse_args()
 src, dst, t, n = synth.config_graph(a.config)
 g = T.Graph(src, dst, t, n)
@@ -25,7 +26,7 @@ for name in a.motifs.split(","):
     mo = T.Motif(mot, bench.DELTA, fine)
     best = None
     for _ in range(a.reps):
-        c = T.tm_count(g, mo)
+        c = T.tm_count(g, mo, grid_ctas=a.grid)
         info = T.tm_last_run_info()
         best = info if best is None or info["mine_ms"] < best["mine_ms"] else best
     tot += best["total_ms"]
