@@ -109,6 +109,7 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     p.src = d.src; p.dst = d.dst; p.off_out = d.off_out; p.off_in = d.off_in; p.rec = d.rec; p.rank = d.rank;
     p.m = (uint32_t)m;
     p.split = (uint32_t)(m + d.n);
+    p.prec = d.prec; p.ptab = d.ptab; p.pmask = d.pmask; p.pbits = d.pbits; p.fmask = d.fmask;
     p.L = mo->L;
     for (uint32_t i = 0; i < mo->L; i++) { p.u[i] = mo->u[i]; p.v[i] = mo->v[i]; }
     if (roots_dev) {

@@ -177,6 +177,46 @@ __global__ void k_sentinels(const uint32_t *off_out, const uint32_t *off_in, uin
     }
 }
 
+__global__ void k_pair_keys(const uint32_t *src, const uint32_t *dst, uint64_t m, int nb, uint64_t *key, uint32_t *val) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+        key[e] = ((uint64_t)src[e] << nb) | dst[e];
+        val[e] = (uint32_t)e;
+    }
+}
+
+// one thread per pair start: insert {key, start, len} (linear probing)
+__global__ void k_pair_insert(const uint64_t *skey, uint64_t m, int nb, uint4 *tab, uint32_t mask, uint32_t *bits,
+                              uint32_t fmask) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = skey[i];
+        if (i > 0 && skey[i - 1] == k) continue;
+        uint64_t j = i + 1;
+        while (j < m && skey[j] == k) j++;
+        const uint64_t src = k >> nb, dst = k & ((1ull << nb) - 1);
+        const uint64_t key = (src << 32) | dst;
+        uint32_t h = (uint32_t)pair_hash(key) & mask;
+        while (true) {
+            unsigned long long *slot = reinterpret_cast<unsigned long long *>(tab + h);
+            if (atomicCAS(slot, ~0ull, (unsigned long long)key) == ~0ull) {
+            const uint32_t b = (uint32_t)(pair_hash(key) >> 32) & fmask;
+            atomicOr(bits + (b >> 5), 1u << (b & 31));
+                tab[h].z = (uint32_t)i;
+                tab[h].w = (uint32_t)(j - i);
+                break;
+            }
+            h = (h + 1) & mask;
+        }
+    }
+}
+
+__global__ void k_count_starts(const uint64_t *skey, uint64_t m, unsigned long long *cnt) {
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        c += (i == 0 || skey[i - 1] != skey[i]) ? 1 : 0;
+    for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
 inline unsigned grid_for(uint64_t m) {
     uint64_t b = (m + 255) / 256;
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * 32));
@@ -188,6 +228,7 @@ cudaError_t dmalloc(T **p, size_t count) { return cudaMalloc((void **)p, std::ma
 void free_graph(DeviceGraph &d) {
     cudaFree(d.src); cudaFree(d.dst); cudaFree(d.t); cudaFree(d.perm);
     cudaFree(d.off_out); cudaFree(d.off_in); cudaFree(d.rec); cudaFree(d.rank);
+    cudaFree(d.prec); cudaFree(d.ptab); cudaFree(d.pbits);
     d = DeviceGraph{};
 }
 
@@ -236,6 +277,57 @@ cudaError_t build_csr(DeviceGraph &d, cudaStream_t s) {
 done:
 #undef TRY
     cudaFree(deg); cudaFree(key); cudaFree(val); cudaFree(kout); cudaFree(vout); cudaFree(flag); cudaFree(tmp);
+    return err;
+}
+
+// Pair index: stable radix sort of the edges by (src, dst), distinct pairs
+// counted, then inserted into the hash table.
+cudaError_t build_pairs(DeviceGraph &d, cudaStream_t s) {
+    const uint64_t m = d.m;
+    uint64_t *key = nullptr, *skey = nullptr;
+    uint32_t *val = nullptr;
+    unsigned long long *cnt = nullptr, hcnt = 0;
+    void *tmp = nullptr;
+    size_t bytes = 0;
+    cudaError_t err;
+    int nb = 1;
+    while (nb < 32 && (1ull << nb) < (uint64_t)d.n) nb++;
+#define TRY(x) do { err = (x); if (err != cudaSuccess) goto done; } while (0)
+    TRY(dmalloc(&d.prec, m + 8));
+    TRY(cudaMemsetAsync(d.prec, 0xff, (m + 8) * 4, s));
+    TRY(dmalloc(&key, m));
+    TRY(dmalloc(&skey, m));
+    TRY(dmalloc(&val, m));
+    TRY(dmalloc(&cnt, 1));
+    TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, skey, val, d.prec, (int64_t)m, 0, 2 * nb, s));
+    TRY(cudaMalloc(&tmp, std::max<size_t>(bytes, 1)));
+    TRY(cudaMemsetAsync(cnt, 0, 8, s));
+    if (m) {
+        k_pair_keys<<<grid_for(m), 256, 0, s>>>(d.src, d.dst, m, nb, key, val);
+        TRY(cub::DeviceRadixSort::SortPairs(tmp, bytes, key, skey, val, d.prec, (int64_t)m, 0, 2 * nb, s));
+        k_count_starts<<<grid_for(m), 256, 0, s>>>(skey, m, cnt);
+    }
+    TRY(cudaMemcpyAsync(&hcnt, cnt, 8, cudaMemcpyDeviceToHost, s));
+    TRY(cudaStreamSynchronize(s));
+    d.npairs = hcnt;
+    {
+        uint64_t cap = 16;
+        while (cap < 2 * hcnt) cap <<= 1;
+        d.pmask = (uint32_t)(cap - 1);
+        TRY(dmalloc(&d.ptab, cap));
+        TRY(cudaMemsetAsync(d.ptab, 0xff, cap * sizeof(uint4), s));
+        uint64_t fb = 1024;
+        while (fb < 8 * hcnt) fb <<= 1;
+        d.fmask = (uint32_t)(fb - 1);
+        TRY(dmalloc(&d.pbits, fb / 32));
+        TRY(cudaMemsetAsync(d.pbits, 0, fb / 8, s));
+    }
+    if (m) k_pair_insert<<<grid_for(m), 256, 0, s>>>(skey, m, nb, d.ptab, d.pmask, d.pbits, d.fmask);
+    TRY(cudaGetLastError());
+    TRY(cudaStreamSynchronize(s));
+done:
+#undef TRY
+    cudaFree(key); cudaFree(skey); cudaFree(val); cudaFree(cnt); cudaFree(tmp);
     return err;
 }
 
@@ -318,6 +410,7 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     if (m) k_gather<<<grid_for(m), 256, 0, s>>>(d.perm, isrc, idst, it, m, d.src, d.dst, d.t);
     TRY(cudaGetLastError());
     TRY(build_csr(d, s));
+    TRY(build_pairs(d, s));
     TRY(cudaStreamSynchronize(s));
 #undef TRY
     if (!on_dev) { cudaFree(isrc); cudaFree(idst); cudaFree(it); }

@@ -31,7 +31,11 @@ namespace tmg {
 constexpr int kCap = 64;             // tasks per level per warp
 constexpr int kWarpsPerBlock = 8;
 constexpr int kRootChunk = 128;      // roots claimed per global atomic
-constexpr int kLeafSectors = 2;      // leaf windows scanned inline up to 8 records
+#ifndef TM_LEAF_SECTORS
+#define TM_LEAF_SECTORS 4
+#endif
+constexpr int kLeafSectors = TM_LEAF_SECTORS;
+      // leaf windows scanned inline up to 8 records
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -115,6 +119,43 @@ __device__ __forceinline__ uint32_t scan_after(const uint64_t *__restrict__ rec,
     }
 }
 
+// first index p in [b, e) with a[p] > key (u32 ids)
+__device__ __forceinline__ uint32_t first_after32(const uint32_t *__restrict__ a, uint32_t b, uint32_t e, uint32_t key) {
+    while (b < e) {
+        const uint32_t mid = b + ((e - b) >> 1);
+        if (__ldg(a + mid) > key) e = mid;
+        else b = mid + 1;
+    }
+    return b;
+}
+
+// The candidate window of a motif edge with both endpoints mapped: the edges
+// a -> b with id in (e, lim], as positions [lo, up) of the pair index.  One
+// hash probe (linear probing) finds the pair; an absent pair is the common
+// case and costs that probe only.
+__device__ __forceinline__ void pair_window(const MineParams &p, uint32_t a, uint32_t b, uint32_t e, uint32_t lim,
+                                            const uint32_t *hf, uint32_t &lo, uint32_t &up) {
+    const uint64_t key = ((uint64_t)a << 32) | b;
+    const uint64_t hh = pair_hash(key);
+    const uint32_t fb = (uint32_t)(hh >> 32) & p.fmask;
+    if (!((__ldg(p.pbits + (fb >> 5)) >> (fb & 31)) & 1u)) {   // certainly absent
+        lo = up = 0;
+        return;
+    }
+    uint32_t h = (uint32_t)hh & p.pmask;
+    uint32_t st = 0, len = 0;
+    while (true) {
+        const uint4 sl = __ldg(p.ptab + h);
+        const uint64_t k = ((uint64_t)sl.y << 32) | sl.x;
+        if (k == key) { st = sl.z; len = sl.w; break; }
+        if (k == ~0ull) break;
+        h = (h + 1) & p.pmask;
+    }
+    if (hf) lim = min(lim, __ldg(hf + e));   // the fine bound, read only for pairs that exist
+    lo = first_after32(p.prec, st, st + len, e);
+    up = first_after32(p.prec, lo, st + len, lim);
+}
+
 __device__ __forceinline__ uint32_t ceil_log2p1(uint32_t len) {  // ceil(log2(len+1))
     return len ? 32 - __clz(len) : 0;
 }
@@ -165,23 +206,21 @@ struct Shape {
     // subtree — the paper's "number of valid mappings at each level"
     // taken one step further: only the φ slots later checks or lists read, the
     // matched ids later window anchors read, and hi only if windows follow.
+    // both endpoints of motif edge l mapped: its candidates are exactly the
+    // edges of one vertex pair, read from the pair index
+    __host__ __device__ constexpr bool pairk(int l) const { return u[l] < nv(l) && v[l] < nv(l); }
     __host__ __device__ constexpr bool keep_phi(int l, int k) const {
         if (k >= nv(l)) return false;
-        for (int q = l; q < L; ++q) {          // structural check of motif edge q
-            const int nb = nv(q);
-            if (u[q] < nb && v[q] < nb) {
-                if ((ldir(q) == 0 ? v[q] : u[q]) == k) return true;
-            } else if (k < nb) {
-                return true;                    // injectivity compares against every mapped vertex
-            }
+        for (int q = l; q < L; ++q)             // injectivity check of a new endpoint
+            if (!pairk(q) && k < nv(q)) return true;
+        for (int q = l + 1; q < L; ++q) {       // vertices of a later window
+            if (pairk(q) ? (u[q] == k || v[q] == k) : lx(q) == k) return true;
         }
-        for (int q = l + 1; q < L; ++q)         // list vertex of a later window
-            if (lx(q) == k) return true;
         return false;
     }
     __host__ __device__ constexpr bool keep_eh(int l, int k) const {
         for (int q = l + 1; q < L; ++q)
-            if (k < l && anc(q) == k) return true;
+            if (k < l && !pairk(q) && anc(q) == k) return true;
         return false;
     }
     __host__ __device__ constexpr bool keep_hi(int l) const { return l + 1 < L; }
@@ -221,6 +260,7 @@ struct PlanC {
     template <int I> __device__ __forceinline__ static constexpr int lx() { constexpr int r = shape_of<CODE>().lx(I); return r; }
     template <int I> __device__ __forceinline__ static constexpr int anc() { constexpr int r = shape_of<CODE>().anc(I); return r; }
     template <int I> __device__ __forceinline__ static constexpr int avar() { constexpr int r = shape_of<CODE>().avar(I); return r; }
+    template <int I> __device__ __forceinline__ static constexpr bool pairk() { constexpr bool r = shape_of<CODE>().pairk(I); return r; }
 };
 
 // Runtime plan: the same kernel body for any prefix-connected motif with
@@ -234,6 +274,7 @@ struct PlanR {
     __host__ __device__ static constexpr bool keep_hi(int) { return true; }
     int L_;
     int u_[kMaxL], v_[kMaxL], nv_[kMaxL + 1], ldir_[kMaxL], lx_[kMaxL], anc_[kMaxL], avar_[kMaxL];
+    bool pairk_[kMaxL];
     __device__ explicit PlanR(const MineParams &p) {
         Shape s{};
         s.L = (int)p.L;
@@ -254,6 +295,7 @@ struct PlanR {
             lx_[i] = live ? s.lx(i) : 0;
             anc_[i] = live ? s.anc(i) : 0;
             avar_[i] = live ? s.avar(i) : 0;
+            pairk_[i] = live && s.pairk(i);
         }
     }
     __device__ __forceinline__ int L() const { return L_; }
@@ -264,6 +306,7 @@ struct PlanR {
     template <int I> __device__ __forceinline__ int lx() const { return lx_[I]; }
     template <int I> __device__ __forceinline__ int anc() const { return anc_[I]; }
     template <int I> __device__ __forceinline__ int avar() const { return avar_[I]; }
+    template <int I> __device__ __forceinline__ bool pairk() const { return pairk_[I]; }
 };
 
 // ------------------------------------------------------- shared-memory layout
@@ -410,7 +453,8 @@ struct Warp {
         uint32_t lo = 0, up = 0;
         if (ok) {
             const uint32_t *hf = p.Hf[NL - 1];
-            const uint32_t lim = hf ? min(hi, __ldg(hf + e)) : hi;   // min(t_root + δ, t_prev + δ_i) as an id
+            uint32_t lim = hi;   // min(t_root + δ, t_prev + δ_i) as an id; H_δi read when needed
+            if (MODE == kStats || !plan.template pairk<NL>()) lim = hf ? min(hi, __ldg(hf + e)) : hi;
             if (MODE == kStats) {
                 // instrumentation of Algorithm 1 itself: shorter list (Q8), two binary searches
                 const int uM = plan.template u<NL>(), vM = plan.template v<NL>(), nb = plan.template nv<NL>();
@@ -428,7 +472,11 @@ struct Warp {
                 }
                 lo = first_after(p.rec, b, en, e);
                 up = first_after(p.rec, lo, en, lim);
-                {   // the window the fast path (below) scans for the same node
+                if (plan.template pairk<NL>()) {   // the window the fast path (below) scans
+                    uint32_t plo, pup;
+                    pair_window(p, xu, xv, e, lim, nullptr, plo, pup);
+                    st.fast_window += pup - plo;
+                } else {
                     const int dir = plan.template ldir<NL>();
                     const uint32_t x = pick(phi, plan.template lx<NL>());
                     const uint32_t fb = __ldg((dir == 0 ? p.off_out : p.off_in) + x);
@@ -440,14 +488,23 @@ struct Warp {
                 st.window += up - lo;
                 st.list += en - b;
                 st.probes += ceil_log2p1(en - b);
+            } else if (plan.template pairk<NL>()) {
+                // both endpoints mapped: the pair's own edge list
+                pair_window(p, pick(phi, plan.template u<NL>()), pick(phi, plan.template v<NL>()), e, hi, hf, lo, up);
+                if (NL + 1 == plan.L()) {   // closing leaf: every edge of the window is a match
+                    leaf_count += up - lo;
+                    if (MODE == kRoots && up > lo) atomicAdd(&p.root_counts[rslot], (unsigned long long)(up - lo));
+                    if (MODE == kEnum)
+                        for (uint32_t q = lo; q < up; q++) emit_one<NE>(eh, e, __ldg(p.prec + q), NL);
+                    lo = up = 0;
+                }
             } else {
                 // window start: one rank load at the anchor edge (the latest
                 // matched edge touching the list vertex), then a short sector
                 // scan to "after e_prev" when the anchor is older than e_prev.
-                // Window end: never searched.  The first sector at lo is read;
-                // if the window ends inside it the task is exact [lo, up),
-                // otherwise it is pushed open-ended (kOpen | lim) and the warp
-                // finds the end while scanning it 32 records at a time.
+                // Window end: the first sector at lo is read (a leaf reads up
+                // to kLeafSectors and counts as it goes); only a window that
+                // runs past them is measured by a gallop.
                 const int dir = plan.template ldir<NL>(), var = plan.template avar<NL>(), j = plan.template anc<NL>();
                 const uint32_t ea = (j == NL - 1) ? e : pick(eh, j);
                 lo = __ldg(p.rank + (size_t)var * p.m + ea);
@@ -601,10 +658,15 @@ struct Warp {
                 else eh[k] = 0u;
             });
             if constexpr (MODE == kRoots) rslot = fld<LV, Lay::rs(LV)>()[jt];
-            const uint64_t rc = __ldg(p.rec + pos);
-            e = (uint32_t)(rc >> 32);
-            w = (uint32_t)rc;
-            ok = accept<LV>(w, pos < p.split, phi);
+            if (MODE != kStats && plan.template pairk<LV>()) {   // a pair window: the edge is the match
+                e = __ldg(p.prec + pos);
+                ok = true;
+            } else {
+                const uint64_t rc = __ldg(p.rec + pos);
+                e = (uint32_t)(rc >> 32);
+                w = (uint32_t)rc;
+                ok = accept<LV>(w, pos < p.split, phi);
+            }
         }
         __syncwarp();
         // consume: pop the fully taken tasks, advance the partially taken one
@@ -647,6 +709,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TM_MIN_BLOCKS) mine_kerne
     uint64_t next = 0, end = 0;
     bool roots_left = true;
 
+#ifdef TM_PHASE_PROFILE
+    unsigned long long prof_cyc[6] = {0, 0, 0, 0, 0, 0}, prof_n[6] = {0, 0, 0, 0, 0, 0};
+#endif
     while (true) {
         int sel = -1;
         // deepest level with a full batch whose child stack has room
@@ -676,13 +741,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TM_MIN_BLOCKS) mine_kerne
             default: break;
         }
 #ifdef TM_PHASE_PROFILE
-        // cycles and steps per selected level (0 = root fetch), scratch[20 + 2*sel]
-        if (lane == 0) {
-            atomicAdd(&p.scratch[20 + 2 * sel], (unsigned long long)(clock64() - t0));
-            atomicAdd(&p.scratch[21 + 2 * sel], 1ull);
+        // cycles and steps per selected level (0 = root fetch), flushed at exit
+        {
+            const unsigned long long dt = (unsigned long long)(clock64() - t0);
+#pragma unroll
+            for (int l = 0; l < 6; l++)
+                if (l == sel) { prof_cyc[l] += dt; prof_n[l] += 1; }
         }
 #endif
     }
+#ifdef TM_PHASE_PROFILE
+    if (lane == 0)
+        for (int l = 0; l < 6; l++)
+            if (prof_n[l]) {
+                atomicAdd(&p.scratch[20 + 2 * l], prof_cyc[l]);
+                atomicAdd(&p.scratch[21 + 2 * l], prof_n[l]);
+            }
+#endif
     unsigned long long tot = W.leaf_count;
     for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(kFull, tot, d);
     tot += W.count;   // lane 0's batch count (other lanes hold 0)

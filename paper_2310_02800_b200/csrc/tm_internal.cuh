@@ -40,7 +40,30 @@ struct DeviceGraph {
     uint32_t *off_out = nullptr, *off_in = nullptr;
     uint64_t *rec = nullptr;
     uint32_t *rank = nullptr;
+    // pair index: prec = edge ids grouped by (src, dst) pair, ascending id in
+    // each group (+8 padding); ptab = open-addressing hash table of the
+    // distinct pairs, slot = {key = src << 32 | dst, start, len}, capacity a
+    // power of two >= 2 x pairs, empty key = ~0.  The candidate list of a
+    // motif edge whose endpoints are both mapped is exactly one pair.
+    uint32_t *prec = nullptr;
+    uint4 *ptab = nullptr;
+    uint32_t pmask = 0;
+    uint64_t npairs = 0;
+    // membership filter of the pairs: one bit per hash bucket, >= 8 buckets
+    // per pair (~12 % false positives), small enough to stay L2-resident, so
+    // an absent pair — the common case when closing a cycle — costs one L2 hit
+    uint32_t *pbits = nullptr;
+    uint32_t fmask = 0;
 };
+
+__host__ __device__ inline uint64_t pair_hash(uint64_t k) {   // splitmix64 finaliser
+    k ^= k >> 30;
+    k *= 0xbf58476d1ce4e5b9ull;
+    k ^= k >> 27;
+    k *= 0x94d049bb133111ebull;
+    k ^= k >> 31;
+    return k;
+}
 
 }  // namespace tmg
 
@@ -79,6 +102,11 @@ struct MineParams {
     const uint32_t *rank;              // DeviceGraph::rank
     uint32_t m;
     uint32_t split;                    // rec positions < split are out-records (m + n)
+    const uint32_t *prec;              // DeviceGraph pair index
+    const uint4 *ptab;
+    uint32_t pmask;
+    const uint32_t *pbits;
+    uint32_t fmask;
     const uint32_t *H;                 // H_δ  (coarse δ-horizon)
     const uint32_t *Hf[kMaxL];         // H_{δ_i} per gap i, nullptr when δ_i = ∞
     uint64_t root_lo, n_roots;         // roots root_lo + [0, n_roots) ...
