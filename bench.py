@@ -228,6 +228,7 @@ def main():
 
     import torch
     import torch.distributed as dist
+    from paper_2310_02800_b200 import multi
     from paper_2310_02800_b200 import tmotif as T
 
     torch.cuda.set_device(local)
@@ -240,9 +241,10 @@ def main():
     m = len(src)
     log(f"[rank {rank}] generated {CONFIG}: m={m} n={n} in {time.time() - t0:.1f}s")
     # contiguous root ranges balanced by the δ-window proxy, + forward δ-halo
+    # (one slice serves all four motifs: reach = max over them of min(δ, Σδ_i) = δ)
     if world > 1:
-        lo, hi = T.tm_partition_plan(t, DELTA, world)
-        a, b, e = int(lo[rank]), int(lo[rank + 1]), int(hi[rank])
+        reach = max(multi.reach(DELTA, motif_fine(x)[1]) for x in MOTIFS)
+        a, b, e = multi.rank_slice(t, reach, world, rank)
     else:
         a, b, e = 0, m, m
     s_src, s_dst, s_t = (np.ascontiguousarray(x[a:e]) for x in (src, dst, t))
@@ -285,13 +287,11 @@ def main():
     if world > 1:
         dist.barrier()
     total_ms = float(sum(step_ms))
-    ct = torch.tensor(counts, dtype=torch.int64, device=dev)
+    counts = multi.allreduce_counts(counts, device=dev)   # the one exchange: combine the counts
     tm_ = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(ct, op=dist.ReduceOp.SUM)       # the one exchange: combine the counts
         dist.all_reduce(tm_, op=dist.ReduceOp.MAX)      # max over ranks
     total_ms = float(tm_.item())
-    counts = [int(x) for x in ct.tolist()]
     roots_per_step = m * len(MOTIFS)
     value = roots_per_step * args.steps / (total_ms / 1000)
     matches_per_s = sum(counts) * args.steps / (total_ms / 1000)

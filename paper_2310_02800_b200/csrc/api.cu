@@ -148,14 +148,14 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     }
     unsigned long long *scratch = nullptr;
     uint32_t *hbuf = nullptr;
-    TM_CUDA_TRY(cudaMallocAsync(&scratch, kScratchWords * sizeof(unsigned long long), s));
-    struct Free { void *a; void *b; void *c; cudaStream_t s; ~Free() { if (a) cudaFreeAsync(a, s); if (b) cudaFreeAsync(b, s); if (c) cudaFreeAsync(c, s); } } fr{scratch, nullptr, nullptr, s};
+    TM_CUDA_TRY(dev_alloc((void **)&scratch, kScratchWords * sizeof(unsigned long long), s));
+    struct Free { void *a; void *b; void *c; cudaStream_t s; ~Free() { dev_free(a, s); dev_free(b, s); dev_free(c, s); } } fr{scratch, nullptr, nullptr, s};
     TM_CUDA_TRY(cudaMemsetAsync(scratch, 0, kScratchWords * sizeof(unsigned long long), s));
     uint64_t *hscr = nullptr;
     if (need_h) {
-        TM_CUDA_TRY(cudaMallocAsync(&hbuf, hv.size() * m * sizeof(uint32_t), s));
+        TM_CUDA_TRY(dev_alloc((void **)&hbuf, hv.size() * m * sizeof(uint32_t), s));
         fr.b = hbuf;
-        TM_CUDA_TRY(cudaMallocAsync(&hscr, horizon_scratch_words(m) * sizeof(uint64_t), s));
+        TM_CUDA_TRY(dev_alloc((void **)&hscr, horizon_scratch_words(m) * sizeof(uint64_t), s));
         fr.c = hscr;
     }
     p.scratch = scratch;
@@ -395,7 +395,7 @@ tm_status tm_enumerate(const tm_graph *g, const tm_motif *mo, const tm_run_opts 
     cudaStream_t s = (cudaStream_t)opt.stream;
     const uint32_t L = mo->L;
     uint32_t *dbuf = buf;
-    if (!opt.buffers_on_device && cap) TM_CUDA_TRY(cudaMalloc(&dbuf, cap * L * sizeof(uint32_t)));
+    if (!opt.buffers_on_device && cap) TM_CUDA_TRY(dev_alloc((void **)&dbuf, cap * L * sizeof(uint32_t), s));
     RunOut r;
     tm_status st = run(g, mo, &opt, kEnum, dbuf, cap, nullptr, 0, nullptr, &r);
     const uint64_t written = std::min(r.count, cap);
@@ -424,7 +424,7 @@ tm_status tm_enumerate(const tm_graph *g, const tm_motif *mo, const tm_run_opts 
             }
         }
     }
-    if (!opt.buffers_on_device && cap) cudaFree(dbuf);
+    if (!opt.buffers_on_device && cap) { dev_free(dbuf, s); cudaStreamSynchronize(s); }
     if (st) return st;
     *n_total = r.count;
     if (n_written) *n_written = written;
@@ -449,8 +449,8 @@ tm_status tm_count_roots(const tm_graph *g, const tm_motif *mo, const tm_run_opt
     if (!opt.buffers_on_device) {
         for (uint64_t i = 0; i < n; i++)
             if (roots[i] >= g->d.m) return fail(TM_EINVAL, "root id >= m");
-        TM_CUDA_TRY(cudaMalloc(&own_r, n * 8));
-        TM_CUDA_TRY(cudaMalloc(&own_c, n * 8));
+        TM_CUDA_TRY(dev_alloc((void **)&own_r, n * 8, s));
+        TM_CUDA_TRY(dev_alloc((void **)&own_c, n * 8, s));
         TM_CUDA_TRY(cudaMemcpyAsync(own_r, roots, n * 8, cudaMemcpyHostToDevice, s));
         droots = own_r;
         dcounts = own_c;
@@ -463,8 +463,9 @@ tm_status tm_count_roots(const tm_graph *g, const tm_motif *mo, const tm_run_opt
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) st = fail(TM_ECUDA, std::string("counts copy: ") + cudaGetErrorString(e));
     }
-    cudaFree(own_r);
-    cudaFree(own_c);
+    dev_free(own_r, s);
+    dev_free(own_c, s);
+    cudaStreamSynchronize(s);
     return st;
 }
 

@@ -3,6 +3,7 @@
 // records, and the per-query δ-horizon arrays.
 #include <cub/cub.cuh>
 
+#include <mutex>
 #include <vector>
 
 #include "tm_internal.cuh"
@@ -223,12 +224,14 @@ inline unsigned grid_for(uint64_t m) {
 }
 
 template <class T>
-cudaError_t dmalloc(T **p, size_t count) { return cudaMalloc((void **)p, std::max<size_t>(count, 1) * sizeof(T)); }
+cudaError_t dmalloc(T **p, size_t count, cudaStream_t s) {
+    return dev_alloc((void **)p, std::max<size_t>(count, 1) * sizeof(T), s);
+}
 
-void free_graph(DeviceGraph &d) {
-    cudaFree(d.src); cudaFree(d.dst); cudaFree(d.t); cudaFree(d.perm);
-    cudaFree(d.off_out); cudaFree(d.off_in); cudaFree(d.rec); cudaFree(d.rank);
-    cudaFree(d.prec); cudaFree(d.ptab); cudaFree(d.pbits);
+void free_graph(DeviceGraph &d, cudaStream_t s) {
+    for (void *q : {(void *)d.src, (void *)d.dst, (void *)d.t, (void *)d.perm, (void *)d.off_out, (void *)d.off_in,
+                    (void *)d.rec, (void *)d.rank, (void *)d.prec, (void *)d.ptab, (void *)d.pbits})
+        dev_free(q, s);
     d = DeviceGraph{};
 }
 
@@ -244,16 +247,16 @@ cudaError_t build_csr(DeviceGraph &d, cudaStream_t s) {
     while (end_bit < 32 && (1ull << end_bit) < (uint64_t)n) end_bit++;
     const uint64_t n2 = 2 * m;
 #define TRY(x) do { err = (x); if (err != cudaSuccess) goto done; } while (0)
-    TRY(dmalloc(&deg, 2 * ((size_t)n + 1)));
-    TRY(dmalloc(&key, n2 + 1));
-    TRY(dmalloc(&val, n2));
-    TRY(dmalloc(&kout, n2));
-    TRY(dmalloc(&vout, n2));
-    TRY(dmalloc(&flag, n2 + 1));
+    TRY(dmalloc(&deg, 2 * ((size_t)n + 1), s));
+    TRY(dmalloc(&key, n2 + 1, s));
+    TRY(dmalloc(&val, n2, s));
+    TRY(dmalloc(&kout, n2, s));
+    TRY(dmalloc(&vout, n2, s));
+    TRY(dmalloc(&flag, n2 + 1, s));
     TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, key, kout, val, vout, (int64_t)n2, 0, end_bit, s));
     TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, deg, d.off_out, (int64_t)n + 1, s));
     TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan2_bytes, flag, key, (int64_t)n2 + 1, s));
-    TRY(cudaMalloc(&tmp, std::max(sort_bytes, std::max(scan_bytes, scan2_bytes))));
+    TRY(dev_alloc(&tmp, std::max(sort_bytes, std::max(scan_bytes, scan2_bytes)), s));
     TRY(cudaMemsetAsync(deg, 0, 2 * ((size_t)n + 1) * 4, s));
     if (m) {
         k_degree<<<grid_for(m), 256, 0, s>>>(d.src, m, deg);
@@ -276,7 +279,7 @@ cudaError_t build_csr(DeviceGraph &d, cudaStream_t s) {
     TRY(cudaStreamSynchronize(s));
 done:
 #undef TRY
-    cudaFree(deg); cudaFree(key); cudaFree(val); cudaFree(kout); cudaFree(vout); cudaFree(flag); cudaFree(tmp);
+    for (void *q : {(void *)deg, (void *)key, (void *)val, (void *)kout, (void *)vout, (void *)flag, tmp}) dev_free(q, s);
     return err;
 }
 
@@ -293,14 +296,14 @@ cudaError_t build_pairs(DeviceGraph &d, cudaStream_t s) {
     int nb = 1;
     while (nb < 32 && (1ull << nb) < (uint64_t)d.n) nb++;
 #define TRY(x) do { err = (x); if (err != cudaSuccess) goto done; } while (0)
-    TRY(dmalloc(&d.prec, m + 8));
+    TRY(dmalloc(&d.prec, m + 8, s));
     TRY(cudaMemsetAsync(d.prec, 0xff, (m + 8) * 4, s));
-    TRY(dmalloc(&key, m));
-    TRY(dmalloc(&skey, m));
-    TRY(dmalloc(&val, m));
-    TRY(dmalloc(&cnt, 1));
+    TRY(dmalloc(&key, m, s));
+    TRY(dmalloc(&skey, m, s));
+    TRY(dmalloc(&val, m, s));
+    TRY(dmalloc(&cnt, 1, s));
     TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, skey, val, d.prec, (int64_t)m, 0, 2 * nb, s));
-    TRY(cudaMalloc(&tmp, std::max<size_t>(bytes, 1)));
+    TRY(dev_alloc(&tmp, std::max<size_t>(bytes, 1), s));
     TRY(cudaMemsetAsync(cnt, 0, 8, s));
     if (m) {
         k_pair_keys<<<grid_for(m), 256, 0, s>>>(d.src, d.dst, m, nb, key, val);
@@ -314,12 +317,12 @@ cudaError_t build_pairs(DeviceGraph &d, cudaStream_t s) {
         uint64_t cap = 16;
         while (cap < 2 * hcnt) cap <<= 1;
         d.pmask = (uint32_t)(cap - 1);
-        TRY(dmalloc(&d.ptab, cap));
+        TRY(dmalloc(&d.ptab, cap, s));
         TRY(cudaMemsetAsync(d.ptab, 0xff, cap * sizeof(uint4), s));
         uint64_t fb = 1024;
         while (fb < 8 * hcnt) fb <<= 1;
         d.fmask = (uint32_t)(fb - 1);
-        TRY(dmalloc(&d.pbits, fb / 32));
+        TRY(dmalloc(&d.pbits, fb / 32, s));
         TRY(cudaMemsetAsync(d.pbits, 0, fb / 8, s));
     }
     if (m) k_pair_insert<<<grid_for(m), 256, 0, s>>>(skey, m, nb, d.ptab, d.pmask, d.pbits, d.fmask);
@@ -327,7 +330,7 @@ cudaError_t build_pairs(DeviceGraph &d, cudaStream_t s) {
     TRY(cudaStreamSynchronize(s));
 done:
 #undef TRY
-    cudaFree(key); cudaFree(skey); cudaFree(val); cudaFree(cnt); cudaFree(tmp);
+    for (void *q : {(void *)key, (void *)skey, (void *)val, (void *)cnt, tmp}) dev_free(q, s);
     return err;
 }
 
@@ -364,20 +367,20 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     tm_status st = TM_OK;
     std::string what;
 #define TRY(x) do { err = (x); if (err != cudaSuccess) { what = #x; goto fail_cuda; } } while (0)
-    TRY(dmalloc(&d.src, m));
-    TRY(dmalloc(&d.dst, m));
-    TRY(dmalloc(&d.t, m));
-    TRY(dmalloc(&d.perm, m));
-    TRY(dmalloc(&d.off_out, (size_t)n + 1));
-    TRY(dmalloc(&d.off_in, (size_t)n + 1));
-    TRY(dmalloc(&d.rec, 2 * (m + n) + 32));   // sentinels + padding: warp reads may run 31 records past a sentinel
+    TRY(dmalloc(&d.src, m, s));
+    TRY(dmalloc(&d.dst, m, s));
+    TRY(dmalloc(&d.t, m, s));
+    TRY(dmalloc(&d.perm, m, s));
+    TRY(dmalloc(&d.off_out, (size_t)n + 1, s));
+    TRY(dmalloc(&d.off_in, (size_t)n + 1, s));
+    TRY(dmalloc(&d.rec, 2 * (m + n) + 32, s));   // sentinels + padding: warp reads may run 31 records past a sentinel
     TRY(cudaMemsetAsync(d.rec, 0xff, (2 * (m + n) + 32) * sizeof(uint64_t), s));
-    TRY(dmalloc(&d.rank, 4 * m));
-    TRY(dmalloc(&flags, 3));
+    TRY(dmalloc(&d.rank, 4 * m, s));
+    TRY(dmalloc(&flags, 3, s));
     if (on_dev) {
         isrc = const_cast<uint32_t *>(src); idst = const_cast<uint32_t *>(dst); it = const_cast<int64_t *>(t);
     } else {
-        TRY(dmalloc(&isrc, m)); TRY(dmalloc(&idst, m)); TRY(dmalloc(&it, m));
+        TRY(dmalloc(&isrc, m, s)); TRY(dmalloc(&idst, m, s)); TRY(dmalloc(&it, m, s));
         if (m) {
             TRY(cudaMemcpyAsync(isrc, src, m * 4, cudaMemcpyHostToDevice, s));
             TRY(cudaMemcpyAsync(idst, dst, m * 4, cudaMemcpyHostToDevice, s));
@@ -396,16 +399,15 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
         // stable LSD radix sort on t (t >= 0, so its bit pattern orders as u64):
         // ties keep input order -> (t, input position) (reading Q1)
         uint32_t *perm2 = nullptr;
-        TRY(dmalloc(&keys_tmp, m));
-        TRY(dmalloc(&perm2, m));
+        TRY(dmalloc(&keys_tmp, m, s));
+        TRY(dmalloc(&perm2, m, s));
         const uint64_t *kin = reinterpret_cast<const uint64_t *>(it);
         uint64_t *kout = reinterpret_cast<uint64_t *>(keys_tmp);
         TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, kout, d.perm, perm2, (int64_t)m, 0, 64, s));
-        TRY(cudaMalloc(&tmp, tmp_bytes));
+        TRY(dev_alloc(&tmp, tmp_bytes, s));
         TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, d.perm, perm2, (int64_t)m, 0, 64, s));
         std::swap(d.perm, perm2);
-        TRY(cudaStreamSynchronize(s));
-        cudaFree(perm2);
+        dev_free(perm2, s);
     }
     if (m) k_gather<<<grid_for(m), 256, 0, s>>>(d.perm, isrc, idst, it, m, d.src, d.dst, d.t);
     TRY(cudaGetLastError());
@@ -413,17 +415,18 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     TRY(build_pairs(d, s));
     TRY(cudaStreamSynchronize(s));
 #undef TRY
-    if (!on_dev) { cudaFree(isrc); cudaFree(idst); cudaFree(it); }
-    cudaFree(keys_tmp); cudaFree(tmp); cudaFree(flags);
+    if (!on_dev) { dev_free(isrc, s); dev_free(idst, s); dev_free(it, s); }
+    dev_free(keys_tmp, s); dev_free(tmp, s); dev_free(flags, s);
     *out = g;
     return TM_OK;
 fail_cuda:
     st = fail(err == cudaErrorMemoryAllocation ? TM_ENOMEM : TM_ECUDA, what + ": " + cudaGetErrorString(err));
 fail_free:
     cudaStreamSynchronize(s);
-    if (!on_dev) { cudaFree(isrc); cudaFree(idst); cudaFree(it); }
-    cudaFree(keys_tmp); cudaFree(tmp); cudaFree(flags);
-    free_graph(d);
+    if (!on_dev) { dev_free(isrc, s); dev_free(idst, s); dev_free(it, s); }
+    dev_free(keys_tmp, s); dev_free(tmp, s); dev_free(flags, s);
+    free_graph(d, s);
+    cudaStreamSynchronize(s);
     delete g;
     return st;
 }
@@ -433,9 +436,41 @@ void graph_destroy(tm_graph *g) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaSetDevice(g->device);
-    free_graph(g->d);
+    cudaDeviceSynchronize();   // no work of any stream may still read the graph
+    free_graph(g->d, nullptr);
     cudaSetDevice(dev);
     delete g;
+}
+
+namespace {
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[64] = {};
+}  // namespace
+
+cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (!g_pool[dev]) {
+            cudaMemPoolProps props = {};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            e = cudaMemPoolCreate(&g_pool[dev], &props);
+            if (e != cudaSuccess) return e;
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool = g_pool[dev];
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+void dev_free(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
 }
 
 }  // namespace tmg

@@ -135,6 +135,12 @@ struct KernelInfo {
 KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised);
 bool is_specialised(uint64_t code);
 
+// Device memory of the library: a per-device CUDA memory pool that keeps
+// freed blocks for reuse (release threshold = max), so per-query buffers
+// (horizons, scratch) and repeated graph builds cost no cudaMalloc/cudaFree.
+cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t s);
+void dev_free(void *p, cudaStream_t s);
+
 // error plumbing
 void set_error(const std::string &msg);
 tm_status fail(tm_status st, const std::string &msg);

@@ -1,0 +1,38 @@
+"""Multi-GPU plumbing (§5.3).
+
+Every search tree touches only edges in [r, H_δ(r)], so ranks
+take contiguous, work-balanced root ranges and hold their roots plus a
+forward δ-halo: no inter-GPU traffic while mining.  The one exchange is the
+sum of the per-rank counts (torch.distributed all-reduce; NCCL on GPUs, gloo
+in the CPU tests).  The split itself is the C-ABI's tm_partition_plan (host
+code, no device needed).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import tmotif as T
+
+
+def reach(delta: int, fine=None) -> int:
+    """Largest possible t(e_L) - t(e_1) of a match: min(δ, Σ δ_i)."""
+    if fine is None or any(f is None or f >= T.DELTA_INF for f in fine):
+        return int(delta)
+    return int(min(delta, sum(int(f) for f in fine)))
+
+
+def rank_slice(t_sorted, reach_s: int, world: int, rank: int, weights=None):
+    """(root_lo, root_hi, edge_hi) of `rank`: it mines roots [root_lo, root_hi)
+    on the sorted edges [root_lo, edge_hi) (its roots + forward halo)."""
+    lo, hi = T.tm_partition_plan(np.ascontiguousarray(t_sorted, np.int64), reach_s, world, weights)
+    return int(lo[rank]), int(lo[rank + 1]), int(hi[rank])
+
+
+def allreduce_counts(counts, device=None):
+    """Sum per-rank count vectors over the default process group (int64)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [int(x) for x in t.tolist()]

@@ -1,0 +1,71 @@
+"""The N>1 path on CPU: two gloo ranks split the roots with the C-ABI's
+partition planner, mine their slice (roots + forward δ-halo) independently
+and combine the counts with one all-reduce — exactly bench.py's multi-GPU
+flow, with the oracle standing in for the device miner (no GPU here)."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2310_02800_b200 import motifs as M
+from paper_2310_02800_b200 import multi, synth
+
+CASES = [("TRI", 3600, None), ("C4", 3600, [1800, 1800, 1800]), ("P3", 3600, [600, 600])]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    src, dst, t, n = synth.config_graph("C1")
+    order = np.lexsort((np.arange(len(t)), t))        # (t, input position): sorted edge ids
+    S, D, Tt = src[order], dst[order], t[order]
+    counts = []
+    for name, delta, fine in CASES:
+        mot = M.get(name)
+        lo, hi, ehi = multi.rank_slice(Tt, multi.reach(delta, fine), world, rank)
+        g = oracle.Graph(S[lo:ehi], D[lo:ehi], Tt[lo:ehi], n)
+        counts.append(g.mine(mot, delta, fine, root_range=(0, hi - lo))["count"])
+    total = multi.allreduce_counts(counts)
+    out[rank] = total
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_counts_allreduce_to_global(world):
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+        assert p.exitcode == 0
+    src, dst, t, n = synth.config_graph("C1")
+    g = oracle.Graph(src, dst, t, n)
+    expect = [g.mine(M.get(name), delta, fine)["count"] for name, delta, fine in CASES]
+    assert all(out[r] == expect for r in range(world))
+    assert sum(expect) > 0
+
+
+def test_reach():
+    assert multi.reach(100, None) == 100
+    assert multi.reach(100, [30, 20]) == 50
+    assert multi.reach(100, [80, 80]) == 100
+    assert multi.reach(100, [None, 5]) == 100
