@@ -10,6 +10,7 @@
 
 #include "catalog.cuh"
 
+
 namespace tmg {
 
 tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m, uint32_t n,
@@ -199,8 +200,13 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
         uint64_t max_useful = (p.n_roots + 31) / 32;
         max_useful = (max_useful + kWarpsPerBlock - 1) / kWarpsPerBlock;
         grid = std::max<uint64_t>(1, std::min(grid, max_useful));
-        ki.fn<<<(unsigned)grid, threads, smem, s>>>(p);
-        TM_CUDA_TRY(cudaGetLastError());
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cfg.numAttrs = 0;
+        TM_CUDA_TRY(cudaLaunchKernelEx(&cfg, ki.fn, p));
         g_info.launches++;
         g_info.grid_ctas = (uint32_t)grid;
         g_info.block_threads = threads;

@@ -199,8 +199,11 @@ __global__ void k_pair_insert(const uint64_t *skey, uint64_t m, int nb, uint4 *t
         while (true) {
             unsigned long long *slot = reinterpret_cast<unsigned long long *>(tab + h);
             if (atomicCAS(slot, ~0ull, (unsigned long long)key) == ~0ull) {
-            const uint32_t b = (uint32_t)(pair_hash(key) >> 32) & fmask;
-            atomicOr(bits + (b >> 5), 1u << (b & 31));
+            const uint64_t hh = pair_hash(key);
+            for (int k = 0; k < (TM_BLOOM_K > 0 ? TM_BLOOM_K : 1); k++) {
+                const uint32_t b = bloom_bit(hh, fmask, k);
+                atomicOr(bits + (b >> 5), 1u << (b & 31));
+            }
                 tab[h].z = (uint32_t)i;
                 tab[h].w = (uint32_t)(j - i);
                 break;
@@ -320,7 +323,7 @@ cudaError_t build_pairs(DeviceGraph &d, cudaStream_t s) {
         TRY(dmalloc(&d.ptab, cap, s));
         TRY(cudaMemsetAsync(d.ptab, 0xff, cap * sizeof(uint4), s));
         uint64_t fb = 1024;
-        while (fb < 8 * hcnt) fb <<= 1;
+        while (fb < (uint64_t)TM_BLOOM_BITS * hcnt) fb <<= 1;
         d.fmask = (uint32_t)(fb - 1);
         TRY(dmalloc(&d.pbits, fb / 32, s));
         TRY(cudaMemsetAsync(d.pbits, 0, fb / 8, s));

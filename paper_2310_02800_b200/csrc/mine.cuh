@@ -31,6 +31,12 @@ namespace tmg {
 constexpr int kCap = 64;             // tasks per level per warp
 constexpr int kWarpsPerBlock = 8;
 constexpr int kRootChunk = 128;      // roots claimed per global atomic
+#ifndef TM_PAIR_LEAF
+#define TM_PAIR_LEAF 0      // closing leaf edges read the pair index (measured: same time, 10x DRAM traffic)
+#endif
+#ifndef TM_PAIR_NONLEAF
+#define TM_PAIR_NONLEAF 1   // closing inner edges read the pair index
+#endif
 #ifndef TM_LEAF_SECTORS
 #define TM_LEAF_SECTORS 4
 #endif
@@ -137,8 +143,7 @@ __device__ __forceinline__ void pair_window(const MineParams &p, uint32_t a, uin
                                             const uint32_t *hf, uint32_t &lo, uint32_t &up) {
     const uint64_t key = ((uint64_t)a << 32) | b;
     const uint64_t hh = pair_hash(key);
-    const uint32_t fb = (uint32_t)(hh >> 32) & p.fmask;
-    if (!((__ldg(p.pbits + (fb >> 5)) >> (fb & 31)) & 1u)) {   // certainly absent
+    if (!pair_maybe(p.pbits, p.fmask, hh)) {   // certainly absent
         lo = up = 0;
         return;
     }
@@ -208,7 +213,9 @@ struct Shape {
     // matched ids later window anchors read, and hi only if windows follow.
     // both endpoints of motif edge l mapped: its candidates are exactly the
     // edges of one vertex pair, read from the pair index
-    __host__ __device__ constexpr bool pairk(int l) const { return u[l] < nv(l) && v[l] < nv(l); }
+    __host__ __device__ constexpr bool pairk(int l) const {
+        return u[l] < nv(l) && v[l] < nv(l) && ((TM_PAIR_LEAF && TM_PAIR_NONLEAF) || (TM_PAIR_LEAF ? l + 1 == L : (TM_PAIR_NONLEAF && l + 1 < L)));
+    }
     __host__ __device__ constexpr bool keep_phi(int l, int k) const {
         if (k >= nv(l)) return false;
         for (int q = l; q < L; ++q)             // injectivity check of a new endpoint

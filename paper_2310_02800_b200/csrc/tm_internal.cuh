@@ -56,6 +56,13 @@ struct DeviceGraph {
     uint32_t fmask = 0;
 };
 
+#ifndef TM_BLOOM_K
+#define TM_BLOOM_K 0        // 0: one bit per pair; k > 0: blocked Bloom, k bits in one 32-byte block
+#endif
+#ifndef TM_BLOOM_BITS
+#define TM_BLOOM_BITS 8     // filter bits per distinct pair (rounded up to a power of two)
+#endif
+
 __host__ __device__ inline uint64_t pair_hash(uint64_t k) {   // splitmix64 finaliser
     k ^= k >> 30;
     k *= 0xbf58476d1ce4e5b9ull;
@@ -64,6 +71,37 @@ __host__ __device__ inline uint64_t pair_hash(uint64_t k) {   // splitmix64 fina
     k ^= k >> 31;
     return k;
 }
+
+// filter bit positions of a pair hash; fmask = filter bits - 1
+__host__ __device__ inline uint32_t bloom_bit(uint64_t h, uint32_t fmask, int i) {
+    if (TM_BLOOM_K == 0) return (uint32_t)(h >> 32) & fmask;
+    const uint32_t block = ((uint32_t)(h >> 32) & fmask) & ~255u;        // 256-bit (32-byte) block
+    return block | (uint32_t)((h >> (8 * i)) & 255u);
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ bool pair_maybe(const uint32_t *bits, uint32_t fmask, uint64_t h) {
+    if (TM_BLOOM_K == 0) {
+        const uint32_t b = bloom_bit(h, fmask, 0);
+        return (__ldg(bits + (b >> 5)) >> (b & 31)) & 1u;
+    }
+    const uint32_t block = bloom_bit(h, fmask, 0) & ~255u;
+    const uint4 *bp = reinterpret_cast<const uint4 *>(bits + (block >> 5));
+    const uint4 q0 = __ldg(bp), q1 = __ldg(bp + 1);
+    const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < (TM_BLOOM_K > 0 ? TM_BLOOM_K : 1); i++) {
+        const uint32_t b = bloom_bit(h, fmask, i) & 255u;
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            if (j == (int)(b >> 5)) word = w[j];
+        ok &= (word >> (b & 31)) & 1u;
+    }
+    return ok;
+}
+#endif
 
 }  // namespace tmg
 

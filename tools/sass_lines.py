@@ -1,6 +1,6 @@
 """Per-source-line warp-stall attribution: joins the SASS stall samples of an
 .ncu-rep kernel with the -lineinfo line table of the same kernel's cubin.
-usage: python tools/sass_lines.py REP KERNEL_REGEX OBJ_FILE MANGLED_SUBSTR [N]"""
+usage: python tools/sass_lines.py REP KERNEL_REGEX OBJ_FILE MANGLED_SUBSTR [N] [SKIP]"""
 import csv
 import io
 import os
@@ -12,8 +12,9 @@ import tempfile
 rep, kre, obj, msub = sys.argv[1:5]
 obj = os.path.abspath(obj)
 N = int(sys.argv[5]) if len(sys.argv) > 5 else 25
+SKIP = sys.argv[6] if len(sys.argv) > 6 else "0"   # launches of KERNEL_REGEX to skip
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name",
-                      f"regex:{kre}", "--launch-count", "1"], capture_output=True, text=True).stdout
+                      f"regex:{kre}", "--launch-skip", SKIP, "--launch-count", "1"], capture_output=True, text=True).stdout
 lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
 rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
