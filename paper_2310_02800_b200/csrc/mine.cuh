@@ -29,7 +29,10 @@
 namespace tmg {
 
 constexpr int kCap = 64;             // tasks per level per warp
-constexpr int kWarpsPerBlock = 8;
+#ifndef TM_WARPS_PER_BLOCK
+#define TM_WARPS_PER_BLOCK 8
+#endif
+constexpr int kWarpsPerBlock = TM_WARPS_PER_BLOCK;
 constexpr int kRootChunk = 128;      // roots claimed per global atomic
 #ifndef TM_PAIR_LEAF
 #define TM_PAIR_LEAF 0      // closing leaf edges read the pair index (measured: same time, 10x DRAM traffic)

@@ -176,9 +176,9 @@ class Graph:
         return self._h
 
     def close(self):
-        if getattr(self, "_h", None):
-            lib().tm_graph_destroy(self._h)
-            self._h = None
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.tm_graph_destroy(self._h)
+        self._h = None
 
     __del__ = close
 
@@ -225,9 +225,9 @@ class Motif:
         return bool(s.value)
 
     def close(self):
-        if getattr(self, "_h", None):
-            lib().tm_motif_destroy(self._h)
-            self._h = None
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.tm_motif_destroy(self._h)
+        self._h = None
 
     __del__ = close
 
