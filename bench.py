@@ -254,13 +254,17 @@ def main():
     rr = (0, b - a)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    balance = [None] * len(MOTIFS)   # load balance of the last step's mining kernels (§8 a8)
+
     def step():
         cs, mine, launches = [], [], 0
-        for mo in motifs:
+        for i, mo in enumerate(motifs):
             cs.append(T.tm_count(g, mo, root_range=rr, stream=stream))
             info = T.tm_last_run_info()
             mine.append(info["mine_ms"])
             launches += info["launches"]
+            balance[i] = {"shared_tasks": info["shared_tasks"], "tail_ms": info["tail_ms"],
+                          "warp_busy": info["warp_busy"]}
         return cs, mine, launches
 
     for _ in range(args.warmup):
@@ -306,7 +310,8 @@ def main():
         avg_ms = mine_ms[i] / args.steps
         per_motif.append({"motif": name, "count": counts[i], "mine_ms": avg_ms,
                           "alg_bytes": bq, "alg_GBps": bq / (avg_ms / 1000) / 1e9,
-                          "search_nodes": sum(st["nodes"][1:L]), "window_sum": st["window_sum"]})
+                          "search_nodes": sum(st["nodes"][1:L]), "window_sum": st["window_sum"],
+                          "load_balance": balance[i]})
     dom = int(np.argmax(mine_ms))
     peak, peak_src = peaks()
     dom_ms = mine_ms[dom] / args.steps

@@ -127,6 +127,13 @@ typedef struct {
     int buffers_on_device;   /* output buffers are device pointers                   */
     uint32_t grid_ctas;      /* 0 = auto (persistent: SMs x resident CTAs)           */
     uint32_t block_threads;  /* 0 = auto                                              */
+    int32_t share;           /* heavy-subtree sharing (load balancing,    */
+                             /* P:815-821): 0 = on: once the root queue is drained,  */
+                             /* busy warps split off the shallowest pending subtrees */
+                             /* (whole tasks or halves of a candidate window) to     */
+                             /* idle warps through a global ticket queue; 1 = off;   */
+                             /* 2 = eager (also leaf-level tasks; a test mode).      */
+                             /* Results are identical in every mode.                 */
 } tm_run_opts;
 
 /* Fill *o with the defaults above. */
@@ -182,6 +189,12 @@ typedef struct {
     uint32_t launches;
     uint32_t grid_ctas;
     uint32_t block_threads;
+    uint64_t shared_tasks;   /* subtrees handed from busy to idle warps (share != 1) */
+    float tail_ms;           /* load balance of the mining kernel: time  */
+                             /* from the first warp finding the root queue empty to  */
+                             /* the last warp's exit                                 */
+    float warp_busy;         /* Σ over warps of time spent searching ÷ (warps ×      */
+                             /* kernel span): 1 = perfectly balanced                 */
 } tm_run_info;
 
 tm_status tm_last_run_info(tm_run_info *out);

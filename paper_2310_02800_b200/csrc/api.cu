@@ -99,6 +99,7 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     tm_run_opts o;
     tm_run_opts_default(&o);
     if (opts) o = *opts;
+    if (o.share < 0 || o.share > 2) return fail(TM_EINVAL, "tm_run_opts.share must be 0, 1 or 2");
     DeviceGuard guard(g->device);
     cudaStream_t s = (cudaStream_t)o.stream;
     const DeviceGraph &d = g->d;
@@ -150,7 +151,11 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     unsigned long long *scratch = nullptr;
     uint32_t *hbuf = nullptr;
     TM_CUDA_TRY(dev_alloc((void **)&scratch, kScratchWords * sizeof(unsigned long long), s));
-    struct Free { void *a; void *b; void *c; cudaStream_t s; ~Free() { dev_free(a, s); dev_free(b, s); dev_free(c, s); } } fr{scratch, nullptr, nullptr, s};
+    struct Free {
+        void *a, *b, *c, *d;
+        cudaStream_t s;
+        ~Free() { dev_free(a, s); dev_free(b, s); dev_free(c, s); dev_free(d, s); }
+    } fr{scratch, nullptr, nullptr, nullptr, s};
     TM_CUDA_TRY(cudaMemsetAsync(scratch, 0, kScratchWords * sizeof(unsigned long long), s));
     uint64_t *hscr = nullptr;
     if (need_h) {
@@ -200,6 +205,22 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
         uint64_t max_useful = (p.n_roots + 31) / 32;
         max_useful = (max_useful + kWarpsPerBlock - 1) / kWarpsPerBlock;
         grid = std::max<uint64_t>(1, std::min(grid, max_useful));
+        // heavy-subtree sharing: idle warps wait for work, so every CTA must
+        // be resident at once (a CTA waiting for a slot would never start)
+        p.share = o.share;
+        if (p.share != 1) {
+            grid = std::min<uint64_t>(grid, (uint64_t)sms * per_sm);
+            p.total_warps = (uint32_t)(grid * kWarpsPerBlock);
+            uint32_t q = 32;
+            while (q < p.total_warps) q <<= 1;
+            p.qmask = q - 1;
+            void *qb = nullptr;
+            TM_CUDA_TRY(dev_alloc(&qb, (size_t)q * (sizeof(unsigned) + kShareWords * sizeof(uint32_t)), s));
+            fr.d = qb;
+            p.qflag = (unsigned *)qb;
+            p.qrec = (uint32_t *)((char *)qb + (size_t)q * sizeof(unsigned));
+            TM_CUDA_TRY(cudaMemsetAsync(p.qflag, 0, (size_t)q * sizeof(unsigned), s));
+        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)grid);
         cfg.blockDim = dim3(threads);
@@ -220,6 +241,15 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     cudaEventElapsedTime(&g_info.mine_ms, ev[1], ev[2]);
     cudaEventElapsedTime(&g_info.total_ms, ev[0], ev[3]);
     out->count = mode == kEnum ? host[2] : host[1];
+    g_info.shared_tasks = host[kShareDone];
+    if (host[kTimeStart] && host[kTimeExit]) {
+        const unsigned long long t0 = ~host[kTimeStart], te = host[kTimeExit];
+        const unsigned long long td = host[kTimeDrain] ? ~host[kTimeDrain] : te;
+        g_info.tail_ms = te > td ? (float)((te - td) * 1e-6) : 0.f;
+        if (te > t0 && g_info.grid_ctas)
+            g_info.warp_busy = (float)(((double)host[kTimeBusy] - (double)host[kTimeWait]) /
+                                       ((double)(te - t0) * g_info.grid_ctas * kWarpsPerBlock));
+    }
 #ifdef TM_PHASE_PROFILE
     fprintf(stderr, "[phase]");
     for (int l = 0; l < 6; l++)

@@ -34,6 +34,25 @@ constexpr int kCap = 64;             // tasks per level per warp
 #endif
 constexpr int kWarpsPerBlock = TM_WARPS_PER_BLOCK;
 constexpr int kRootChunk = 128;      // roots claimed per global atomic
+#ifndef TM_SHARE
+#define TM_SHARE 1          // heavy-subtree sharing compiled in (tm_run_opts.share)
+#endif
+#ifndef TM_TIMING
+#define TM_TIMING 1         // load-balance timing (tm_run_info.tail_ms / warp_busy)
+#endif
+#ifndef TM_SHARE_MIN
+#define TM_SHARE_MIN 128
+#endif
+constexpr int kShareMin = TM_SHARE_MIN;   // smallest window handed to an idle warp (share = 0)
+#ifndef TM_SHARE_POLL
+#define TM_SHARE_POLL 16
+#endif
+constexpr uint32_t kSharePoll = TM_SHARE_POLL;   // iterations between reads of the idle counter (power of 2)
+constexpr unsigned kShareStop = 0xFFFFFFFFu;     // flag value: the search is complete
+#ifndef TM_SHARE_SLEEP
+#define TM_SHARE_SLEEP 2048
+#endif
+constexpr unsigned kShareSleepMax = TM_SHARE_SLEEP;   // ns, longest back-off of a waiting warp
 #ifndef TM_PAIR_LEAF
 #define TM_PAIR_LEAF 0      // closing leaf edges read the pair index (measured: same time, 10x DRAM traffic)
 #endif
@@ -46,6 +65,12 @@ constexpr int kRootChunk = 128;      // roots claimed per global atomic
 constexpr int kLeafSectors = TM_LEAF_SECTORS;
       // leaf windows scanned inline up to 8 records
 constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
@@ -590,18 +615,19 @@ struct Warp {
 
     // Take up to 32 roots from the global cursor and bind motif edge 1 to them
     // (the root level maps motif edge 1 onto every graph edge).
-    __device__ __forceinline__ bool fetch_roots(uint64_t &next, uint64_t &end) {
+    // next/end: this warp's claimed root slots (u32: n_roots <= m < 2^31)
+    __device__ __forceinline__ bool fetch_roots(uint32_t &next, uint32_t &end) {
         if (next >= end) {
             unsigned long long b = 0;
             if (lane == 0) b = atomicAdd(&p.scratch[0], (unsigned long long)kRootChunk);
             b = __shfl_sync(kFull, b, 0);
             if (b >= p.n_roots) return false;
-            next = b;
-            end = min((uint64_t)(b + kRootChunk), (uint64_t)p.n_roots);
+            next = (uint32_t)b;
+            end = (uint32_t)min((uint64_t)(b + kRootChunk), (uint64_t)p.n_roots);
         }
-        const uint64_t slot = next + lane;
+        const uint32_t slot = next + lane;
         bool ok = slot < end;
-        next = min((uint64_t)(next + 32), end);
+        next = min(next + 32u, end);
         uint32_t r = 0, a = 0, bb = 0;
         if (ok) {
             r = (uint32_t)(p.roots ? p.roots[slot] : p.root_lo + slot);
@@ -702,13 +728,212 @@ struct Warp {
             push<LV + 1>(ok, e, hi, phi2, eh, rslot);
         }
     }
+
+    // ------------------------------------------ heavy-subtree sharing (§8 a8)
+    // The paper's tail-warp work redistribution (abort the tail
+    // warps, dump their contexts, relaunch) done inside the persistent kernel,
+    // with no relaunch.  Once the root queue is drained, a warp that sees idle
+    // warps hands one pending subtree to one of them: the bottom task of its
+    // shallowest non-leaf level (the oldest, least explored subtree), or, when
+    // that level holds a single task, the upper half of its cached candidate
+    // window (sub-tree-level parallelism).  A task is
+    // self-contained (its level's SoA fields: window, φ, hi, matched ids), so
+    // the receiver continues exactly the search the donor would have run.
+    // Hand-over: the donor claims an idle warp (decrements the idle counter),
+    // takes a ticket d, writes the record to ring slot d and publishes it with
+    // flag = d + 1; idle warps take tickets in the same order and wait on
+    // their own slot's flag.  The warp whose arrival makes every warp idle
+    // writes kShareStop into the flags of the unserved tickets: the search is
+    // complete.  Only pieces of >= kShareMin candidates are handed over, and
+    // busy warps read the idle counter every kSharePoll iterations (measured:
+    // per-iteration reads of one counter by thousands of warps congest its L2
+    // slice, profiles/r01_experiments.md).
+
+    // hand over task j of level LV (whole, or the upper half of its window)
+    template <int LV>
+    __device__ __forceinline__ void give(uint32_t *rec, bool split, uint32_t j) {
+        using Lay = Layout<Plan, MODE>;
+        constexpr int F = Lay::fields(LV);
+        static_assert(F < kShareWords, "task record too large");
+        uint32_t *base = ws + Lay::off(LV);   // word f of task j at base[f * kCap + j]
+        const uint32_t lo = base[j], up = base[kCap + j];
+        const uint32_t mid = lo + ((up - lo) >> 1);
+        uint32_t val = lane < F ? base[lane * kCap + j] : 0u;
+        if (split && lane == 0) val = mid;               // handed over: [mid, up)
+        if (lane == kShareWords - 1) val = (uint32_t)LV;
+        __stcg(rec + lane, val);
+        __syncwarp();
+        if (split) {
+            if (lane == 0) base[kCap + j] = mid;          // kept: [lo, mid)
+            cand[LV] -= up - mid;
+        } else {                                          // the top task fills slot j
+            const uint32_t top = ntask[LV] - 1;
+            if (lane < F) base[lane * kCap + j] = base[lane * kCap + top];
+            ntask[LV] = top;
+            cand[LV] -= up - lo;
+        }
+        __syncwarp();
+    }
+
+    template <int LV>
+    __device__ __forceinline__ void take(uint32_t val) {
+        using Lay = Layout<Plan, MODE>;
+        constexpr int F = Lay::fields(LV);
+        uint32_t *base = ws + Lay::off(LV);
+        const uint32_t slot = ntask[LV];
+        if (lane < F) base[lane * kCap + slot] = val;
+        const uint32_t lo = __shfl_sync(kFull, val, 0), up = __shfl_sync(kFull, val, 1);
+        ntask[LV] = slot + 1;
+        cand[LV] += up - lo;
+        __syncwarp();
+    }
+
+    // Called when idle warps were seen: hand over one subtree if there is one
+    // worth handing (non-leaf levels; every level in eager mode).
+    __device__ void try_share() {
+        int lv = -1;
+        bool split = false;
+        uint32_t jb = 0;
+        const int L = plan.L();
+        sfor<LM>([&](auto lc) {
+            constexpr int l = decltype(lc)::value;
+            if constexpr (l >= 1) {
+                if (lv < 0 && l < L && (l + 1 < L || p.share == 2) && ntask[l] > 0) {
+                    // the level's task with the largest remaining window (lane i
+                    // looks at tasks i and i + 32); only pieces of >= kShareMin
+                    // candidates are worth a hand-over (a short window is cheaper
+                    // to finish than to move; eager mode: any)
+                    const uint32_t *base = ws + Layout<Plan, MODE>::off(l);
+                    const uint32_t n = ntask[l];
+                    const uint32_t wa = (uint32_t)lane < n ? base[kCap + lane] - base[lane] : 0u;
+                    const uint32_t wb = (uint32_t)lane + 32 < n ? base[kCap + lane + 32] - base[lane + 32] : 0u;
+                    const uint32_t wl = max(wa, wb);
+                    const uint32_t wmax = __reduce_max_sync(kFull, wl);
+                    const int src = __ffs(__ballot_sync(kFull, wl == wmax)) - 1;
+                    const uint32_t j = __shfl_sync(kFull, wb > wa ? lane + 32u : (uint32_t)lane, src);
+                    const uint32_t smin = p.share == 2 ? 1u : (uint32_t)kShareMin;
+                    if (wmax >= 2 * smin) {
+                        lv = l; jb = j; split = true;
+                    } else if (n >= 2 && wmax >= smin) {
+                        lv = l; jb = j;
+                    }
+                }
+            }
+        });
+        if (lv < 0) return;
+        unsigned long long d = 0;
+        int ok = 0;
+        if (lane == 0) {
+            int *idle = reinterpret_cast<int *>(p.scratch + kShareIdle);
+            if (atomicSub(idle, 1) > 0) {
+                ok = 1;
+                d = atomicAdd(p.scratch + kShareTail, 1ull);
+                volatile unsigned *f = p.qflag + (d & p.qmask);
+                while (*f != 0u) __nanosleep(32);   // the slot's previous record is still being read
+            } else {
+                atomicAdd(idle, 1);                  // nobody to give to after all
+            }
+        }
+        if (!__shfl_sync(kFull, ok, 0)) return;
+        d = __shfl_sync(kFull, d, 0);
+        uint32_t *rec = p.qrec + (size_t)(d & p.qmask) * kShareWords;
+        switch (lv) {
+            case 1: if constexpr (LM > 1) give<1>(rec, split, jb); break;
+            case 2: if constexpr (LM > 2) give<2>(rec, split, jb); break;
+            case 3: if constexpr (LM > 3) give<3>(rec, split, jb); break;
+            case 4: if constexpr (LM > 4) give<4>(rec, split, jb); break;
+            case 5: if constexpr (LM > 5) give<5>(rec, split, jb); break;
+            default: break;
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            atomicExch(p.qflag + (d & p.qmask), (unsigned)(d + 1));
+            atomicAdd(p.scratch + kShareDone, 1ull);
+        }
+    }
+
+    // This warp has no work left: wait for a handed-over subtree.  Returns
+    // false when every warp is idle (the search is complete).
+    __device__ bool receive() {
+        int got = 0, last = 0;
+        unsigned long long r = 0;
+        if (lane == 0) {
+            r = atomicAdd(p.scratch + kShareHead, 1ull);
+            __threadfence();   // the ticket is taken before this warp counts as idle
+            const int before = atomicAdd(reinterpret_cast<int *>(p.scratch + kShareIdle), 1);
+            last = before + 1 == (int)p.total_warps;
+            if (!last) {
+                // wait on this ticket's own flag only (no shared hot spot)
+                volatile unsigned *f = p.qflag + (r & p.qmask);
+                unsigned ns = 64;
+                while (true) {
+                    const unsigned v = *f;
+                    if (v == (unsigned)(r + 1)) { got = 1; break; }
+                    if (v == kShareStop) break;
+                    __nanosleep(ns);
+                    if (ns < kShareSleepMax) ns <<= 1;
+                }
+                __threadfence();
+            }
+        }
+        if (__shfl_sync(kFull, last, 0)) {
+            // every warp is idle and none can become busy again: release the
+            // waiting ones (their tickets are the unserved [tail, head)), one
+            // flag per lane
+            __threadfence();
+            r = __shfl_sync(kFull, r, 0);
+            const unsigned long long tl = *reinterpret_cast<volatile unsigned long long *>(p.scratch + kShareTail);
+            const unsigned long long hd = *reinterpret_cast<volatile unsigned long long *>(p.scratch + kShareHead);
+            for (unsigned long long d = tl + lane; d < hd; d += 32)
+                if (d != r) p.qflag[d & p.qmask] = kShareStop;
+            return false;
+        }
+        if (!__shfl_sync(kFull, got, 0)) return false;
+        r = __shfl_sync(kFull, r, 0);
+        const uint32_t *rec = p.qrec + (size_t)(r & p.qmask) * kShareWords;
+        const uint32_t val = __ldcg(rec + lane);
+        const int lv = (int)__shfl_sync(kFull, val, kShareWords - 1);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicExch(p.qflag + (r & p.qmask), 0u);   // the slot is free again
+        switch (lv) {
+            case 1: if constexpr (LM > 1) take<1>(val); break;
+            case 2: if constexpr (LM > 2) take<2>(val); break;
+            case 3: if constexpr (LM > 3) take<3>(val); break;
+            case 4: if constexpr (LM > 4) take<4>(val); break;
+            case 5: if constexpr (LM > 5) take<5>(val); break;
+            default: break;
+        }
+        return true;
+    }
 };
 
-#ifndef TM_MIN_BLOCKS
-#define TM_MIN_BLOCKS 1
+// Resident CTAs per SM the register allocator must allow for specialised
+// counting kernels: <= 3 motif edges fit 40 registers (6 CTAs of 256 threads
+// per SM), 4 edges 48 (5 CTAs), 5 edges 64 (4 CTAs), all without spills
+// (ptxas -v); left alone, ptxas lands just above each step and the grid
+// loses a CTA per SM.  Everything else: the allocator's choice.
+#ifndef TM_MIN_BLOCKS3
+#define TM_MIN_BLOCKS3 6
+#endif
+#ifndef TM_MIN_BLOCKS4
+#define TM_MIN_BLOCKS4 5
+#endif
+#ifndef TM_MIN_BLOCKS5
+#define TM_MIN_BLOCKS5 4
 #endif
 template <class Plan, int MODE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, TM_MIN_BLOCKS) mine_kernel(const MineParams p) {
+struct MinBlocks {
+    static constexpr int value = 1;
+};
+template <uint64_t CODE>
+struct MinBlocks<PlanC<CODE>, kCount> {
+    static constexpr int value = PlanC<CODE>::kL <= 3 ? TM_MIN_BLOCKS3 : PlanC<CODE>::kL == 4 ? TM_MIN_BLOCKS4 : TM_MIN_BLOCKS5;
+};
+
+template <class Plan, int MODE>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, (MinBlocks<Plan, MODE>::value)) mine_kernel(const MineParams p) {
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int LM = Plan::kL;
@@ -716,13 +941,33 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TM_MIN_BLOCKS) mine_kerne
     const Plan plan(p);
     Warp<Plan, MODE> W(p, plan, ws, lane);
     const int L = plan.L();
-    uint64_t next = 0, end = 0;
+    uint32_t next = 0, end = 0;
+    uint32_t iter = 0;   // iterations, for the idle-counter poll
     bool roots_left = true;
+    // load-balance instrumentation (tm_run_info.tail_ms / warp_busy): this
+    // warp's start in 64-ns ticks (u32: wraps after 275 s, differences stay
+    // exact); time spent waiting for handed-over work is added in receive
+    uint32_t t_start = 0;
+    if (TM_TIMING && lane == 0) {
+        const unsigned long long t = globaltimer_ns();
+        t_start = (uint32_t)(t >> 6);
+        atomicMax(p.scratch + kTimeStart, ~t);
+    }
 
 #ifdef TM_PHASE_PROFILE
     unsigned long long prof_cyc[6] = {0, 0, 0, 0, 0, 0}, prof_n[6] = {0, 0, 0, 0, 0, 0};
 #endif
+    const bool share = TM_SHARE && p.share != 1;
     while (true) {
+        // every kSharePoll iterations read the idle counter and, if warps wait
+        // (so the root queue is drained), hand one subtree over.  A warp deep
+        // in a heavy tree never returns to the root queue itself, so this must
+        // not wait for its own fetch to fail.
+        if (share && (++iter & (kSharePoll - 1)) == 0) {
+            int idle = 0;
+            if (lane == 0) idle = *reinterpret_cast<volatile int *>(p.scratch + kShareIdle);
+            if (__shfl_sync(kFull, idle, 0) > 0) W.try_share();
+        }
         int sel = -1;
         // deepest level with a full batch whose child stack has room
 #pragma unroll
@@ -737,12 +982,24 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TM_MIN_BLOCKS) mine_kerne
                     if (sel < 0 && l < L && W.ntask[l] > 0 && (l == L - 1 || W.ntask[l + 1 <= LM ? l + 1 : LM] < 32)) sel = l;
             }
         }
-        if (sel < 0) break;
+        if (sel < 0) {
+            if (share) {
+                const unsigned long long tw = TM_TIMING ? globaltimer_ns() : 0;
+                const bool more = W.receive();
+                if (TM_TIMING && lane == 0) atomicAdd(p.scratch + kTimeWait, globaltimer_ns() - tw);
+                if (more) continue;
+            }
+            break;
+        }
 #ifdef TM_PHASE_PROFILE
         const long long t0 = clock64();
 #endif
         switch (sel) {
-            case 0: roots_left = W.fetch_roots(next, end); break;
+            case 0:
+                roots_left = W.fetch_roots(next, end);
+                if (TM_TIMING && !roots_left && lane == 0)   // the root queue is drained: the tail starts
+                    atomicMax(p.scratch + kTimeDrain, ~globaltimer_ns());
+                break;
             case 1: if constexpr (LM > 1) W.template expand<1>(); break;
             case 2: if constexpr (LM > 2) W.template expand<2>(); break;
             case 3: if constexpr (LM > 3) W.template expand<3>(); break;
@@ -768,6 +1025,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TM_MIN_BLOCKS) mine_kerne
                 atomicAdd(&p.scratch[21 + 2 * l], prof_n[l]);
             }
 #endif
+    if (TM_TIMING && lane == 0) {
+        const unsigned long long te = globaltimer_ns();
+        atomicMax(p.scratch + kTimeExit, te);
+        atomicAdd(p.scratch + kTimeBusy, (unsigned long long)((uint32_t)(te >> 6) - t_start) << 6);
+    }
     unsigned long long tot = W.leaf_count;
     for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(kFull, tot, d);
     tot += W.count;   // lane 0's batch count (other lanes hold 0)

@@ -154,12 +154,29 @@ struct MineParams {
     uint32_t *enum_buf;
     uint64_t cap;
     uint32_t id_offset;
+    // heavy-subtree sharing (tm_run_opts::share): a ring of
+    // qmask+1 task records of kShareWords words and their ticket flags
+    // (0 = empty, ticket+1 = filled for that ticket); tickets and the idle
+    // counter live in scratch[kShareTail..kShareDone]
+    int share;
+    unsigned int *qflag;
+    uint32_t *qrec;
+    uint32_t qmask;
+    uint32_t total_warps;
     // runtime plan (generic kernel)
     uint32_t L;
     uint8_t u[kMaxL], v[kMaxL];
 };
 
-constexpr int kScratchWords = 40;
+constexpr int kScratchWords = 48;
+// load-balance timing (globaltimer ns): max(~start) over warps, max(~drain)
+// (the first warp to find the root queue empty), max(exit), Σ per-warp
+// (exit - start), Σ time spent waiting for handed-over work
+constexpr int kTimeStart = 40, kTimeDrain = 41, kTimeExit = 42, kTimeBusy = 43, kTimeWait = 44;
+// scratch words of the sharing queue: donor tickets, receiver tickets, idle
+// warps (an int in the low half), subtrees handed over
+constexpr int kShareTail = 3, kShareHead = 4, kShareIdle = 5, kShareDone = 6;
+constexpr int kShareWords = 32;   // u32 words per shared task record (fields + level in word 31)
 constexpr int kStatsBase = 8;   // scratch[8 + l] nodes[l], [16] window, [17] list, [18] probes, [19] fast window
 
 using MineKernel = void (*)(MineParams);

@@ -164,3 +164,31 @@ def tiny_graph(seed: int, n: int = 8, m: int = 40, tmax: int = 30, p_self: float
     dst[s] = src[s]
     t = rng.integers(0, tmax + 1, m).astype(np.int64)
     return src, dst, t, n
+
+
+def burst_graph(seed: int, n: int = 2000, m_bg: int = 10000, span: int = 86400 * 7, bursts: int = 2,
+                core: int = 48, burst_len: int = 600):
+    """Skewed workload for the load-balancing row (§8 a8; "the top
+    0.1% of the search trees constitute 34% of explored tree nodes"):
+    a uniform random background plus `bursts` dense cores — `core` vertices
+    exchanging every ordered pair once within `burst_len` seconds — so the
+    few roots inside a core own almost all of the search work.  Input order
+    random; timestamps integer seconds."""
+    rng = np.random.default_rng(seed)
+    src = [rng.integers(0, n, m_bg)]
+    dst = [rng.integers(0, n, m_bg)]
+    t = [rng.integers(0, span, m_bg)]
+    for _ in range(bursts):
+        vs = rng.choice(n, core, replace=False)
+        a, b = np.meshgrid(vs, vs, indexing="ij")
+        keep = a != b
+        a, b = a[keep], b[keep]
+        t0 = int(rng.integers(0, span - burst_len))
+        src.append(a)
+        dst.append(b)
+        t.append(t0 + rng.integers(0, burst_len, a.shape[0]))
+    src = np.concatenate(src).astype(np.uint32)
+    dst = np.concatenate(dst).astype(np.uint32)
+    t = np.concatenate(t).astype(np.int64)
+    p = rng.permutation(src.shape[0])
+    return src[p], dst[p], t[p], n

@@ -41,7 +41,7 @@ class GraphOpts(ctypes.Structure):
 class RunOpts(ctypes.Structure):
     _fields_ = [("stream", _P), ("root_lo", _u64), ("root_hi", _u64), ("edge_id_offset", _u64),
                 ("canonical", _i32), ("buffers_on_device", _i32), ("grid_ctas", _u32),
-                ("block_threads", _u32)]
+                ("block_threads", _u32), ("share", _i32)]
 
 
 class SearchStats(ctypes.Structure):
@@ -51,7 +51,8 @@ class SearchStats(ctypes.Structure):
 
 class RunInfo(ctypes.Structure):
     _fields_ = [("horizon_ms", _f32), ("mine_ms", _f32), ("total_ms", _f32), ("launches", _u32),
-                ("grid_ctas", _u32), ("block_threads", _u32)]
+                ("grid_ctas", _u32), ("block_threads", _u32), ("shared_tasks", _u64),
+                ("tail_ms", _f32), ("warp_busy", _f32)]
 
 
 _lib = None
@@ -128,7 +129,8 @@ def _stream_handle(stream):
 
 
 def run_opts(stream=None, root_range=None, edge_id_offset=0, canonical=False, buffers_on_device=False,
-             grid_ctas=0) -> RunOpts:
+             grid_ctas=0, share=0) -> RunOpts:
+    """share: heavy-subtree sharing, 0 on (default), 1 off, 2 eager (tm_run_opts)."""
     o = RunOpts()
     lib().tm_run_opts_default(ctypes.byref(o))
     o.stream = _stream_handle(stream)
@@ -138,6 +140,7 @@ def run_opts(stream=None, root_range=None, edge_id_offset=0, canonical=False, bu
     o.canonical = int(bool(canonical))
     o.buffers_on_device = int(bool(buffers_on_device))
     o.grid_ctas = int(grid_ctas)
+    o.share = int(share)
     return o
 
 
@@ -281,7 +284,8 @@ def tm_last_run_info() -> dict:
     r = RunInfo()
     _check(lib().tm_last_run_info(ctypes.byref(r)))
     return {"horizon_ms": r.horizon_ms, "mine_ms": r.mine_ms, "total_ms": r.total_ms, "launches": r.launches,
-            "grid_ctas": r.grid_ctas, "block_threads": r.block_threads}
+            "grid_ctas": r.grid_ctas, "block_threads": r.block_threads, "shared_tasks": r.shared_tasks,
+            "tail_ms": r.tail_ms, "warp_busy": r.warp_busy}
 
 
 def tm_partition_plan(t_sorted, delta: int, P: int, weights=None):

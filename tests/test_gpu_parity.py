@@ -297,3 +297,45 @@ def test_bursts_and_equal_timestamps():
     for motif, delta, fine in ((M.TRI, 0, None), (M.PATH2, 50, None), (M.C4, 500, [0, 100, 100]),
                                (M.STAR3, 1000, None)):
         check_case(src, dst, t, n, motif, delta, fine, rows=False, roots=False)
+
+
+# ------------------------------------------- heavy-subtree sharing (§8 a8)
+@pytest.mark.parametrize("share", [0, 1, 2])
+def test_heavy_subtree_sharing(share):
+    """Skewed graph (two dense bursts own most of the search work):
+    every sharing mode (0 on, 1 off, 2 eager) gives the oracle's counts,
+    per-root counts, enumeration and search-tree counters, and the sharing
+    modes really hand subtrees over."""
+    src, dst, t, n = synth.burst_graph(231002806)
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    allr = np.arange(len(src), dtype=np.uint64)
+    shared = 0
+    cases = [("TRI", None), ("C4", None), ("P3", [600, 600]), ("DIA", [None, 900, None, 1800]),
+             ("TT", None)]
+    for name, fine in cases:
+        motif = M.get(name)
+        exp = og.mine(motif, 3600, fine, enumerate_=True)
+        mo = T.Motif(motif, 3600, fine)
+        assert T.tm_count(g, mo, share=share) == exp["count"], name
+        shared += T.tm_last_run_info()["shared_tasks"]
+        rows, n_total = T.tm_enumerate(g, mo, exp["count"], canonical=True, share=share)
+        shared += T.tm_last_run_info()["shared_tasks"]
+        assert n_total == exp["n_total"]
+        assert np.array_equal(rows, np.asarray(exp["rows"], np.uint32).reshape(-1, len(motif)))
+        pr = og.mine(motif, 3600, fine, roots=allr, per_root=True)["per_root"]
+        assert np.array_equal(T.tm_count_roots(g, mo, allr, share=share), pr), name
+        st = T.tm_search_stats_run(g, mo, share=share)
+        assert st["nodes"][:len(motif)] == exp["stats"]["nodes"][:len(motif)]
+        assert st["window_sum"] == exp["stats"]["window_sum"]
+    if share == 1:
+        assert shared == 0
+    elif share == 2:   # eager: hands over even short windows, so this small graph exercises it
+        assert shared > 0
+
+
+def test_sharing_rejects_bad_mode():
+    g = T.Graph(np.array([0, 1], np.uint32), np.array([1, 2], np.uint32), np.array([0, 1], np.int64), 3)
+    mo = T.Motif(M.get("P3")[:2], 10)
+    with pytest.raises(T.TMotifError):
+        T.tm_count(g, mo, share=3)
