@@ -179,8 +179,23 @@ typedef struct {
 tm_status tm_search_stats_run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o,
                               tm_search_stats *out);
 
+/* Fused census of the 36 two/three-node three-edge motifs (SURVEY.md §8(f)
+ * N1, config C2): counts[a*6 + b] = the δ-temporal count of the
+ * motif (0->1, E[a], E[b]), E = [0->1, 1->0, 0->2, 2->0, 1->2, 2->1], for the
+ * roots of o's root range — the same 36 numbers as 36 tm_count calls, from
+ * one traversal that shares the level-2 windows across all 36 motifs and the
+ * level-3 windows across the six with the same second edge.
+ *   delta : δ >= 0 or TM_DELTA_INF
+ *   fine  : NULL, or 2 entries δ_1, δ_2 (gaps e1-e2, e2-e3), each >= 0 or
+ *           TM_DELTA_INF
+ *   counts: host, 36 entries (written on success)
+ * Synchronous on o->stream.  Errors: TM_EINVAL (null argument, δ < 0,
+ * δ_i < 0), TM_ENOMEM, TM_ECUDA.  tm_last_run_info reports its times. */
+tm_status tm_census36(const tm_graph *g, int64_t delta, const int64_t *fine, const tm_run_opts *o,
+                      uint64_t *counts);
+
 /* Device times (ms, CUDA events on o->stream) of the calling thread's last
- * tm_count / tm_enumerate / tm_count_roots: horizon construction, the mining
+ * tm_count / tm_enumerate / tm_count_roots / tm_census36: horizon construction, the mining
  * kernel, and the whole call.  launches: kernels this library launched in it. */
 typedef struct {
     float horizon_ms;

@@ -505,6 +505,87 @@ tm_status tm_count_roots(const tm_graph *g, const tm_motif *mo, const tm_run_opt
     return st;
 }
 
+tm_status tm_census36(const tm_graph *g, int64_t delta, const int64_t *fine, const tm_run_opts *o,
+                      uint64_t *counts) {
+    g_err.clear();
+    if (!g || !counts) return fail(TM_EINVAL, "null argument");
+    if (delta < 0) return fail(TM_EINVAL, "delta < 0");
+    if (fine && (fine[0] < 0 || fine[1] < 0)) return fail(TM_EINVAL, "fine delta < 0");
+    tm_run_opts opt;
+    tm_run_opts_default(&opt);
+    if (o) opt = *o;
+    DeviceGuard guard(g->device);
+    cudaStream_t s = (cudaStream_t)opt.stream;
+    const DeviceGraph &d = g->d;
+    const uint64_t m = d.m;
+    g_info = tm_run_info{};
+    CensusParams p;
+    std::memset(&p, 0, sizeof p);
+    p.src = d.src; p.dst = d.dst; p.rec = d.rec; p.rank = d.rank; p.m = (uint32_t)m;
+    const uint64_t hi = std::min<uint64_t>(opt.root_hi, m), lo = std::min<uint64_t>(opt.root_lo, hi);
+    p.root_lo = lo;
+    p.n_roots = hi - lo;
+    // distinct horizons: δ, then δ_1, δ_2 when finite and < δ (a larger gap bound never binds)
+    std::vector<int64_t> hv{delta};
+    int gi[2] = {-1, -1};
+    for (int i = 0; i < 2 && fine; i++) {
+        if (fine[i] == TM_DELTA_INF || fine[i] >= delta) continue;
+        auto it = std::find(hv.begin(), hv.end(), fine[i]);
+        gi[i] = (int)(it - hv.begin());
+        if (it == hv.end()) hv.push_back(fine[i]);
+    }
+    unsigned long long *dcounts = nullptr;
+    uint32_t *hbuf = nullptr;
+    uint64_t *hscr = nullptr;
+    TM_CUDA_TRY(dev_alloc((void **)&dcounts, 36 * sizeof(unsigned long long), s));
+    struct Free {
+        void *a, *b, *c;
+        cudaStream_t s;
+        ~Free() { dev_free(a, s); dev_free(b, s); dev_free(c, s); }
+    } fr{dcounts, nullptr, nullptr, s};
+    TM_CUDA_TRY(cudaMemsetAsync(dcounts, 0, 36 * sizeof(unsigned long long), s));
+    p.counts = dcounts;
+    cudaEvent_t ev[4] = {};
+    for (auto &e : ev) TM_CUDA_TRY(cudaEventCreate(&e));
+    struct EvFree { cudaEvent_t *e; ~EvFree() { for (int i = 0; i < 4; i++) if (e[i]) cudaEventDestroy(e[i]); } } evf{ev};
+    TM_CUDA_TRY(cudaEventRecord(ev[0], s));
+    if (p.n_roots > 0) {
+        TM_CUDA_TRY(dev_alloc((void **)&hbuf, hv.size() * m * sizeof(uint32_t), s));
+        fr.b = hbuf;
+        TM_CUDA_TRY(dev_alloc((void **)&hscr, horizon_scratch_words(m) * sizeof(uint64_t), s));
+        fr.c = hscr;
+        for (size_t i = 0; i < hv.size(); i++) {
+            TM_CUDA_TRY(build_horizon(d, hv[i], hbuf + i * m, hscr, s));
+            g_info.launches += 2;
+        }
+        p.H = hbuf;
+        p.Hf0 = gi[0] >= 0 ? hbuf + (size_t)gi[0] * m : nullptr;
+        p.Hf1 = gi[1] >= 0 ? hbuf + (size_t)gi[1] * m : nullptr;
+    }
+    TM_CUDA_TRY(cudaEventRecord(ev[1], s));
+    if (p.n_roots > 0) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        TM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const uint64_t want = (p.n_roots + 255) / 256;
+        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms * 8));
+        TM_CUDA_TRY(launch_census36(p, grid, s));
+        g_info.launches++;
+        g_info.grid_ctas = (uint32_t)grid;
+        g_info.block_threads = 256;
+    }
+    TM_CUDA_TRY(cudaEventRecord(ev[2], s));
+    unsigned long long host[36];
+    TM_CUDA_TRY(cudaMemcpyAsync(host, dcounts, sizeof host, cudaMemcpyDeviceToHost, s));
+    TM_CUDA_TRY(cudaEventRecord(ev[3], s));
+    TM_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaEventElapsedTime(&g_info.horizon_ms, ev[0], ev[1]);
+    cudaEventElapsedTime(&g_info.mine_ms, ev[1], ev[2]);
+    cudaEventElapsedTime(&g_info.total_ms, ev[0], ev[3]);
+    for (int i = 0; i < 36; i++) counts[i] = host[i];
+    return TM_OK;
+}
+
 tm_status tm_last_run_info(tm_run_info *out) {
     if (!out) return fail(TM_EINVAL, "out is null");
     *out = g_info;

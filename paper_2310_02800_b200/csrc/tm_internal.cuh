@@ -179,6 +179,19 @@ constexpr int kShareTail = 3, kShareHead = 4, kShareIdle = 5, kShareDone = 6;
 constexpr int kShareWords = 32;   // u32 words per shared task record (fields + level in word 31)
 constexpr int kStatsBase = 8;   // scratch[8 + l] nodes[l], [16] window, [17] list, [18] probes, [19] fast window
 
+// Parameters of the fused 36-motif census (census.cu).
+struct CensusParams {
+    const uint32_t *src, *dst;
+    const uint64_t *rec;
+    const uint32_t *rank;
+    uint32_t m;
+    const uint32_t *H;              // H_δ
+    const uint32_t *Hf0, *Hf1;      // H_δ1, H_δ2 or nullptr (δ_i = ∞ or >= δ)
+    uint64_t root_lo, n_roots;
+    unsigned long long *counts;     // 36 bins, index a * 6 + b
+};
+cudaError_t launch_census36(const CensusParams &p, int grid, cudaStream_t s);
+
 using MineKernel = void (*)(MineParams);
 
 struct KernelInfo {

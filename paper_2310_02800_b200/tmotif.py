@@ -74,6 +74,7 @@ SIGNATURES = [
                             ctypes.POINTER(_u64)]),
     ("tm_count_roots", _i32, [_P, _P, ctypes.POINTER(RunOpts), _P, _u64, _P]),
     ("tm_search_stats_run", _i32, [_P, _P, ctypes.POINTER(RunOpts), ctypes.POINTER(SearchStats)]),
+    ("tm_census36", _i32, [_P, _i64, _P, ctypes.POINTER(RunOpts), _P]),
     ("tm_last_run_info", _i32, [ctypes.POINTER(RunInfo)]),
     ("tm_partition_plan", _i32, [_P, _u64, _i64, _u32, _P, _P, _P]),
     ("tm_last_error", ctypes.c_char_p, []),
@@ -278,6 +279,20 @@ def tm_search_stats_run(g: Graph, mo: Motif, **opts) -> dict:
     _check(lib().tm_search_stats_run(g.handle, mo.handle, ctypes.byref(o), ctypes.byref(s)))
     return {"nodes": list(s.nodes), "window_sum": s.window_sum, "list_sum": s.list_sum,
             "probe_sum": s.probe_sum, "matches": s.matches, "fast_window_sum": s.fast_window_sum}
+
+
+def tm_census36(g: Graph, delta: int, fine=None, **opts) -> np.ndarray:
+    """36 counts, index a*6+b = motif (0→1, E6[a], E6[b]) (motifs.P36 order)."""
+    counts = np.zeros(36, np.uint64)
+    fa = None
+    if fine is not None:
+        fa = np.array([DELTA_INF if f is None else int(f) for f in fine], np.int64)
+        if fa.shape[0] != 2:
+            raise ValueError("fine needs 2 entries")
+    o = run_opts(**opts)
+    _check(lib().tm_census36(g.handle, int(delta), None if fa is None else _host_ptr(fa), ctypes.byref(o),
+                             _host_ptr(counts)))
+    return counts
 
 
 def tm_last_run_info() -> dict:

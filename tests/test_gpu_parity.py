@@ -339,3 +339,52 @@ def test_sharing_rejects_bad_mode():
     mo = T.Motif(M.get("P3")[:2], 10)
     with pytest.raises(T.TMotifError):
         T.tm_count(g, mo, share=3)
+
+
+# ------------------------------------------------ fused 36-motif census (N1)
+def test_census36_C2_vs_oracle():
+    """tm_census36 on config C2 equals the oracle's 36 per-motif counts
+    (bit-exact), whole graph and as a sum over root ranges."""
+    src, dst, t, n = synth.config_graph("C2")
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    exp = np.array([og.mine(M.P36[k], 3600)["count"] for k in range(36)], np.uint64)
+    got = T.tm_census36(g, 3600)
+    assert np.array_equal(got, exp)
+    cuts = [0, 1000, 150_000, 150_001, len(src)]
+    parts = sum(T.tm_census36(g, 3600, root_range=(cuts[i], cuts[i + 1])) for i in range(len(cuts) - 1))
+    assert np.array_equal(parts, exp)
+    # with per-gap bounds, against the oracle's fine-δ counts
+    fine = [600, 1800]
+    exp_f = np.array([og.mine(M.P36[k], 3600, fine)["count"] for k in range(36)], np.uint64)
+    assert np.array_equal(T.tm_census36(g, 3600, fine), exp_f)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_census36_tiny_random_vs_oracle(seed):
+    rng = random.Random(1000 + seed)
+    for k in range(12):
+        src, dst, t, n = synth.tiny_graph(seed * 50 + k, n=rng.randint(2, 7), m=rng.randint(0, 120),
+                                          tmax=rng.randint(5, 60))
+        delta = rng.choice([0, 3, 10, 25, INF])
+        fine = None if rng.random() < 0.4 else [rng.choice([0, 2, 7, INF]), rng.choice([0, 4, 12, INF])]
+        og = oracle.Graph(src, dst, t, n)
+        g = T.Graph(src, dst, t, n)
+        exp = np.array([og.mine(M.P36[i], delta, fine)["count"] for i in range(36)], np.uint64)
+        assert np.array_equal(T.tm_census36(g, delta, fine), exp), (seed, k, delta, fine)
+        # and against the per-motif CUDA path
+        if k % 4 == 0:
+            got = [T.tm_count(g, T.Motif(M.P36[i], delta, fine)) for i in range(36)]
+            assert np.array_equal(np.array(got, np.uint64), exp)
+
+
+def test_census36_bursts_and_errors():
+    src, dst, t, n = synth.burst_graph(231002807, n=300, m_bg=3000, core=24)
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    exp = np.array([og.mine(M.P36[i], 3600)["count"] for i in range(36)], np.uint64)
+    assert np.array_equal(T.tm_census36(g, 3600), exp)
+    with pytest.raises(T.TMotifError):
+        T.tm_census36(g, -1)
+    empty = T.Graph(np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.int64), 4)
+    assert not T.tm_census36(empty, 10).any()
