@@ -35,10 +35,24 @@ sys.path.insert(0, ROOT)
 from paper_2310_02800_b200 import motifs as M  # noqa: E402
 from paper_2310_02800_b200 import synth  # noqa: E402
 
+# BASELINE.json configs the bench can run: C4 (default: the config the metric's
+# 1/2/4/8-GPU scaling is quoted on) and C5 (the billion-edge one, drawn and
+# mined in C5_PARTS time slices with δ-halos; rank r takes parts r, r+N, ...)
+CONFIGS = {
+    "C4": {"motifs": ["P3", "TRI", "C4", "DIA"], "delta": 86400, "fine": 21600, "index": 3},
+    "C5": {"motifs": ["TRI", "C4"], "delta": 3600, "fine": None, "index": 4},
+}
+C5_PARTS = 8
 CONFIG = "C4"
-MOTIFS = ["P3", "TRI", "C4", "DIA"]
-DELTA = 86400
-FINE = 21600
+MOTIFS = CONFIGS[CONFIG]["motifs"]
+DELTA = CONFIGS[CONFIG]["delta"]
+FINE = CONFIGS[CONFIG]["fine"]
+
+
+def select_config(name):
+    global CONFIG, MOTIFS, DELTA, FINE
+    CONFIG = name
+    MOTIFS, DELTA, FINE = CONFIGS[name]["motifs"], CONFIGS[name]["delta"], CONFIGS[name]["fine"]
 METRIC = "root edges/s"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -48,19 +62,25 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def workload_config(world):
-    spec = synth.SPECS[CONFIG]
-    return {"workload": f"{CONFIG} {spec.name.split(' ', 1)[1]} synthetic temporal graph (BASELINE.json configs[3])",
-            "n": spec.n, "m": spec.m, "motifs": MOTIFS, "delta_s": DELTA, "fine_delta_s": FINE,
-            "mode": "count", "generator": {"alpha": spec.alpha, "cap": spec.cap, "mu": spec.mu, "beta_s": spec.beta,
-                                           "seed": synth.SEED_BASE + 3},
-            "partition": f"{world} contiguous root ranges + forward δ-halo" if world > 1 else "whole graph",
-            "cache": "graph 2.3 GB > 126 MB L2; L2 flushed (256 MiB write) between timed steps"}
+def workload_config(world, m=None):
+    spec = synth.C5 if CONFIG == "C5" else synth.SPECS[CONFIG]
+    idx = CONFIGS[CONFIG]["index"]
+    cfg = {"workload": f"{CONFIG} {spec.name.split(' ', 1)[1]} synthetic temporal graph (BASELINE.json configs[{idx}])",
+           "n": spec.n, "m": m or spec.m, "motifs": MOTIFS, "delta_s": DELTA, "fine_delta_s": FINE,
+           "mode": "count", "generator": {"alpha": spec.alpha, "cap": spec.cap, "mu": spec.mu, "beta_s": spec.beta,
+                                          "seed": synth.SEED_BASE + idx},
+           "partition": f"{world} contiguous root ranges + forward δ-halo" if world > 1 else "whole graph",
+           "cache": "graph 2.3 GB > 126 MB L2; L2 flushed (256 MiB write) between timed steps"}
+    if CONFIG == "C5":
+        cfg["partition"] = (f"{C5_PARTS} equal time slices + forward δ-halo, rank r holds slices r, r+{world}, ...; "
+                            f"each slice drawn, built and timed resident in turn")
+        cfg["cache"] = "each slice's graph ~17 GB > 126 MB L2; L2 flushed (256 MiB write) between timed steps"
+    return cfg
 
 
 def motif_fine(name):
     mot = M.get(name)
-    return mot, [FINE] * (len(mot) - 1)
+    return mot, (None if FINE is None else [FINE] * (len(mot) - 1))
 
 
 def balgo_bytes(stats, n_roots, L, fine=True):
@@ -138,14 +158,14 @@ def peaks():
 
 
 # ------------------------------------------------------------------ oracle
-def oracle_sample(src, dst, t, n, budget_s, seed=0):
+def oracle_sample(src, dst, t, n, budget_s, seed=0, n_roots=None):
     """The oracle (Algorithm 1 in plain C, OpenMP over roots) as it stands,
     on all host cores, on a seeded uniform sample of roots of the same
     workload, sized to ~budget_s of CPU work.  Returns root edges/s etc."""
     import oracle
     threads = os.cpu_count() or 1
     og = oracle.Graph(src, dst, t, n)
-    m = len(src)
+    m = len(src) if n_roots is None else n_roots
     rng = np.random.default_rng(seed)
     k = 1 << 14
     spent, roots_done, matches, t_total = 0.0, 0, 0, 0.0
@@ -163,17 +183,21 @@ def oracle_sample(src, dst, t, n, budget_s, seed=0):
         k = int(min(m, k * max(2.0, min(8.0, (budget_s - t_total) / max(dt, 1e-3)))))
     return {"value": roots_done / t_total, "unit": "root edges/s", "cores": threads, "kind": "oracle",
             "sample": f"{roots_done // len(MOTIFS)} uniformly sampled roots (seeded) x {len(MOTIFS)} motifs of the "
-                      f"{CONFIG} workload, {t_total:.1f} s on {threads} threads",
+                      f"{CONFIG} workload{' (time slice 0)' if CONFIG == 'C5' else ''}, {t_total:.1f} s on "
+                      f"{threads} threads",
             "matches_per_s": matches / t_total}
 
 
 def run_reference(args):
     """--impl reference: the oracle on the host cores, same config/metric."""
-    src, dst, t, n = synth.config_graph(CONFIG)
+    if CONFIG == "C5":
+        src, dst, t, n, m = synth.c5_rank_slice(0, C5_PARTS, DELTA)
+    else:
+        src, dst, t, n = synth.config_graph(CONFIG)
+        m = len(src)
     import oracle
     threads = os.cpu_count() or 1
     og = oracle.Graph(src, dst, t, n)
-    m = len(src)
     per_step = 1 << 18
     rng = np.random.default_rng(1)
 
@@ -197,7 +221,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "root edges/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1000 / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i64",
-            "data": "synthetic", "config": workload_config(1), "matches_per_s": matches / dt,
+            "data": "synthetic", "config": workload_config(args.gpus), "matches_per_s": matches / dt,
             "cpu_baseline": {"value": v, "unit": "root edges/s", "cores": threads, "kind": "oracle",
                              "sample": f"each step {per_step} uniformly sampled roots x {len(MOTIFS)} motifs"},
             "e2e": {"value": v, "unit": "root edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -215,7 +239,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C4")
     args = ap.parse_args()
+    select_config(args.config)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -236,27 +262,33 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    t0 = time.time()
-    src, dst, t, n = synth.config_graph(CONFIG)
-    m = len(src)
-    log(f"[rank {rank}] generated {CONFIG}: m={m} n={n} in {time.time() - t0:.1f}s")
-    # contiguous root ranges balanced by the δ-window proxy, + forward δ-halo
-    # (one slice serves all four motifs: reach = max over them of min(δ, Σδ_i) = δ)
-    if world > 1:
-        reach = max(multi.reach(DELTA, motif_fine(x)[1]) for x in MOTIFS)
-        a, b, e = multi.rank_slice(t, reach, world, rank)
-    else:
-        a, b, e = 0, m, m
-    s_src, s_dst, s_t = (np.ascontiguousarray(x[a:e]) for x in (src, dst, t))
-    stream = torch.cuda.Stream(dev)
-    g = T.Graph(s_src, s_dst, s_t, n, device=local, stream=stream)
-    motifs = [T.Motif(*motif_fine(name)[:1], DELTA, motif_fine(name)[1]) for name in MOTIFS]
-    rr = (0, b - a)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    # ---- this rank's parts: (src, dst, t, n, root range); edges beyond the
+    # root range are the forward δ-halo
+    def parts():
+        if CONFIG == "C5":
+            for part in range(rank, C5_PARTS, world):
+                t0 = time.time()
+                s_, d_, t_, n_, nr = synth.c5_rank_slice(part, C5_PARTS, DELTA)
+                log(f"[rank {rank}] C5 slice {part}/{C5_PARTS}: m={len(s_)} roots={nr} in {time.time() - t0:.1f}s")
+                yield s_, d_, t_, n_, (0, nr)
+            return
+        t0 = time.time()
+        src, dst, t, n = synth.config_graph(CONFIG)
+        m = len(src)
+        log(f"[rank {rank}] generated {CONFIG}: m={m} n={n} in {time.time() - t0:.1f}s")
+        if world > 1:   # contiguous root ranges balanced by the δ-window proxy, + forward δ-halo
+            reach = max(multi.reach(DELTA, motif_fine(x)[1]) for x in MOTIFS)
+            a, b, e = multi.rank_slice(t, reach, world, rank)
+        else:
+            a, b, e = 0, m, m
+        yield tuple(np.ascontiguousarray(x[a:e]) for x in (src, dst, t)) + (n, (0, b - a))
 
+    stream = torch.cuda.Stream(dev)
+    motifs = [T.Motif(*motif_fine(name)[:1], DELTA, motif_fine(name)[1]) for name in MOTIFS]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     balance = [None] * len(MOTIFS)   # load balance of the last step's mining kernels (§8 a8)
 
-    def step():
+    def step(g, rr):
         cs, mine, launches = [], [], 0
         for i, mo in enumerate(motifs):
             cs.append(T.tm_count(g, mo, root_range=rr, stream=stream))
@@ -267,55 +299,97 @@ def main():
                           "warp_busy": info["warp_busy"]}
         return cs, mine, launches
 
-    for _ in range(args.warmup):
-        step()
+    def timed(fn):
+        with torch.cuda.stream(stream):
+            flush.zero_()                      # untimed L2 flush between steps
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1), out
+
+    step_ms = np.zeros(args.steps)
+    mine_ms = np.zeros(len(MOTIFS))
+    counts = np.zeros(len(MOTIFS), np.int64)
+    launches, my_roots, part0 = 0, 0, None
+    e2e_ms, h2d = 0.0, 0
+    with ClockSampler(local) as clk:
+        for pi, (s_src, s_dst, s_t, n, rr) in enumerate(parts()):
+            g = T.Graph(s_src, s_dst, s_t, n, device=local, stream=stream)
+            for _ in range(args.warmup):
+                step(g, rr)
+            if world > 1 and (CONFIG != "C5" or C5_PARTS % world == 0):   # same part count on every rank
+                dist.barrier()
+            torch.cuda.synchronize()
+            for k in range(args.steps):
+                ms, (cs, mm, nl) = timed(lambda: step(g, rr))
+                step_ms[k] += ms
+                launches += nl
+                if k == 0:
+                    mine_ms += np.array(mm)
+                    counts += np.array(cs, np.int64)
+            my_roots += rr[1] - rr[0]
+            if pi == 0:   # roofline inputs (untimed instrumentation runs) from this rank's first part
+                stats = [T.tm_search_stats_run(g, mo, root_range=rr, stream=stream) for mo in motifs]
+                part0 = {"roots": rr[1] - rr[0], "mine_ms": [None] * len(MOTIFS), "stats": stats,
+                         "arrays": (s_src, s_dst, s_t, n, rr[1])}
+                _, (_, mm0, _) = timed(lambda: step(g, rr))
+                part0["mine_ms"] = mm0
+                part0["balance"] = [dict(x) for x in balance]
+            g.close()
+            del g
+            # ---- end to end through the public API from pinned host memory
+            if not args.no_e2e:
+                ph = [torch.from_numpy(x).pin_memory() for x in (s_src, s_dst, s_t)]
+                hs, hd, ht = (x.numpy() for x in ph)
+
+                def e2e_step():
+                    gg = T.Graph(hs, hd, ht, n, device=local, stream=stream)
+                    cs = [T.tm_count(gg, mo, root_range=rr, stream=stream) for mo in motifs]
+                    gg.close()
+                    return cs
+
+                for _ in range(2):   # warm-up: grows the library's memory pool to a graph's size
+                    e2e_step()
+                torch.cuda.synchronize()
+                for _ in range(args.e2e_steps):
+                    e2e_ms += timed(e2e_step)[0]
+                h2d += int(sum(x.numel() * x.element_size() for x in ph))
+                del ph, hs, hd, ht
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    step_ms, mine_ms, launches, counts = [], np.zeros(len(MOTIFS)), 0, None
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.zero_()                      # untimed L2 flush between steps
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            cs, mm, nl = step()
-            e1.record(stream)
-            e1.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-            mine_ms += np.array(mm)
-            launches += nl
-            counts = cs
-        torch.cuda.synchronize()
+    total_ms = float(step_ms.sum())
+    counts = multi.allreduce_counts(counts.tolist(), device=dev)   # the one exchange: combine the counts
+    tot = torch.tensor([total_ms, e2e_ms, float(my_roots), float(h2d)], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.barrier()
-    total_ms = float(sum(step_ms))
-    counts = multi.allreduce_counts(counts, device=dev)   # the one exchange: combine the counts
-    tm_ = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tm_, op=dist.ReduceOp.MAX)      # max over ranks
-    total_ms = float(tm_.item())
-    roots_per_step = m * len(MOTIFS)
+        mx = tot[:2].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)   # max over ranks
+        sm = tot[2:].clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        tot = torch.cat([mx, sm])
+    total_ms, e2e_ms, all_roots, h2d_all = (float(x) for x in tot.tolist())
+    roots_per_step = all_roots * len(MOTIFS)
     value = roots_per_step * args.steps / (total_ms / 1000)
     matches_per_s = sum(counts) * args.steps / (total_ms / 1000)
 
-    # ---- roofline of the dominant kernel (untimed instrumentation runs)
+    # ---- roofline of the dominant kernel: algorithmic bytes per launch (the
+    # method's own instrumentation on this rank's first part) ÷ its CUDA-event time
     bytes_q, per_motif = [], []
-    for i, (name, mo) in enumerate(zip(MOTIFS, motifs)):
-        st = T.tm_search_stats_run(g, mo, root_range=rr, stream=stream)
+    for i, name in enumerate(MOTIFS):
         L = len(M.get(name))
-        bq = balgo_bytes(st, b - a, L)
+        bq = balgo_bytes(part0["stats"][i], part0["roots"], L, fine=FINE is not None)
         bytes_q.append(bq)
-        avg_ms = mine_ms[i] / args.steps
-        per_motif.append({"motif": name, "count": counts[i], "mine_ms": avg_ms,
-                          "alg_bytes": bq, "alg_GBps": bq / (avg_ms / 1000) / 1e9,
-                          "search_nodes": sum(st["nodes"][1:L]), "window_sum": st["window_sum"],
-                          "load_balance": balance[i]})
-    dom = int(np.argmax(mine_ms))
+        ms = part0["mine_ms"][i]
+        per_motif.append({"motif": name, "count": counts[i], "mine_ms": ms,
+                          "alg_bytes": bq, "alg_GBps": bq / (ms / 1000) / 1e9,
+                          "search_nodes": sum(part0["stats"][i]["nodes"][1:L]),
+                          "window_sum": part0["stats"][i]["window_sum"], "load_balance": part0["balance"][i]})
+    dom = int(np.argmax(part0["mine_ms"]))
     peak, peak_src = peaks()
-    dom_ms = mine_ms[dom] / args.steps
-    achieved = bytes_q[dom] / (dom_ms / 1000) / 1e9
+    achieved = bytes_q[dom] / (part0["mine_ms"][dom] / 1000) / 1e9
     traffic = None
     try:
         nc = json.load(open(NCU_SUMMARY))
@@ -326,56 +400,29 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": f"mine_kernel<PlanC<{MOTIFS[dom]}>, kCount>",
                 "peak_source": peak_src, "per_motif": per_motif,
-                "mine_share_of_step": float(mine_ms.sum() / sum(step_ms))}
-
-    # ---- end to end through the public API from pinned host memory
+                "mine_share_of_step": float(mine_ms.sum() / (total_ms / args.steps))}
     e2e = None
     if not args.no_e2e:
-        ph = [torch.from_numpy(x).pin_memory() for x in (s_src, s_dst, s_t)]
-        hs, hd, ht = (x.numpy() for x in ph)
-
-        def e2e_step():
-            gg = T.Graph(hs, hd, ht, n, device=local, stream=stream)
-            cs = [T.tm_count(gg, mo, root_range=rr, stream=stream) for mo in motifs]
-            gg.close()
-            return cs
-
-        for _ in range(2):   # warm-up: grows the library's memory pool to a graph's size
-            e2e_step()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        ee = []
-        for _ in range(args.e2e_steps):
-            with torch.cuda.stream(stream):
-                flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            e2e_step()
-            e1.record(stream)
-            e1.synchronize()
-            ee.append(e0.elapsed_time(e1))
-        te = torch.tensor([sum(ee)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": roots_per_step * args.e2e_steps / (float(te.item()) / 1000), "unit": "root edges/s",
-               "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in ph)) * world,
-               "d2h_bytes_per_step": 256 * len(MOTIFS) * world,
-               "includes": "graph load from pinned host (H2D + validate + sort + CSR build) + 4 queries + count read-back"}
+        e2e = {"value": roots_per_step * args.e2e_steps / (e2e_ms / 1000), "unit": "root edges/s",
+               "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": 256 * len(MOTIFS) * world,
+               "includes": f"graph load from pinned host (H2D + validate + sort + CSR build) + {len(MOTIFS)} "
+                           f"queries + count read-back" + (f", for each of the {C5_PARTS} C5 slices"
+                                                           if CONFIG == "C5" else "")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_sample(src, dst, t, n, args.cpu_seconds)
+        s_src, s_dst, s_t, n, nr = part0["arrays"]
+        cpu = oracle_sample(s_src, s_dst, s_t, n, args.cpu_seconds, n_roots=nr)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "root edges/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-                "config": workload_config(world), "matches_per_s": matches_per_s, "counts": dict(zip(MOTIFS, counts)),
+                "config": workload_config(world, int(all_roots) if CONFIG == "C5" else None),
+                "matches_per_s": matches_per_s, "counts": dict(zip(MOTIFS, counts)),
                 "hbm_pct_of_peak": roofline["frac"] * 100, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk.summary(), "gpu_launches": int(launches) * world,
-                "gpu_launches_note": "per rank: H_δ + H_δi horizon kernels and one mining kernel per query"}
+                "gpu_launches_note": "per rank: H_δ (+ H_δi) horizon kernels and one mining kernel per query"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -192,3 +192,107 @@ def burst_graph(seed: int, n: int = 2000, m_bg: int = 10000, span: int = 86400 *
     t = np.concatenate(t).astype(np.int64)
     p = rng.permutation(src.shape[0])
     return src[p], dst[p], t[p], n
+
+
+# ---------------------------------------------------------------- config C5
+# Billion-edge eth-shaped graph (BASELINE.json configs[4]; SURVEY.md §8(d):
+# n = 2^27, m ≈ 2e9, span 3.58 y, μ = 3.4, β = 10 min; α = 1.0, cap 0.3 %: calibrated
+# with the oracle on a 1-day slice, to ~1e6 4-cycles per day
+# against the eth dataset's 6.4e9 in 3.58 y).
+# Too large to draw whole on one host, so it is generated in *time slices*:
+# sessions are grouped into C5_BLOCKS blocks by start time, block b drawn
+# from its own PCG64 stream (seed, b) and starting inside
+# [b, b+1) · span / C5_BLOCKS.  A slice [ta, tb) draws only the blocks that
+# can reach it (sessions last <= C5_MAX_SESSION s) and keeps the events in
+# it, so every rank of a multi-GPU run draws exactly its own roots plus its
+# δ-halo, and any two slices agree on the events they share.  Global order:
+# (t, session, event).  m is ≈ 2e9 (the session count is fixed, events per
+# session are random); vertex activity is the capped power law sampled in
+# closed form: the top K ranks (share > cap) are drawn uniformly with mass
+# K·cap, the rest by the inverse CDF of the continuous (r+1)^-α law, and
+# ranks are scattered over the ids by the bijection r ↦ (r·φ32 + 12345) mod n.
+C5 = GraphSpec("C5 billion-edge eth-shaped", 1 << 27, 2_000_000_000, int(3.58 * YEAR), 3.4, 1.0, 0.003, 600.0)
+C5_BLOCKS = 8192
+C5_MAX_SESSION = DAY
+C5_MAX_EVENTS = 63
+
+
+def _capped_zipf(rng, k, n, alpha, cap):
+    # continuous (r+1)^-α law on ranks via G(x) = x^(1-α)/(1-α) (ln x at α = 1)
+    if abs(alpha - 1.0) < 1e-12:
+        G, Ginv = np.log, np.exp
+    else:
+        G = lambda x: np.power(x, 1.0 - alpha) / (1.0 - alpha)          # noqa: E731
+        Ginv = lambda y: np.power(y * (1.0 - alpha), 1.0 / (1.0 - alpha))  # noqa: E731
+    r = np.arange(1, 4097, dtype=np.float64)
+    H = float(G(n + 0.5) - G(0.5))                                      # ≈ Σ_{r=1..n} r^-α
+    K = int(((r ** -alpha) / H > cap).sum())
+    head_mass = K * cap
+    u = rng.random(k)
+    head = u < head_mass
+    out = np.empty(k, np.int64)
+    if K:
+        out[head] = np.minimum((u[head] / cap).astype(np.int64), K - 1)
+    lo, hi = G(K + 0.5), G(n + 0.5)
+    x = rng.random(int((~head).sum()))
+    out[~head] = np.clip(np.floor(Ginv(lo + x * (hi - lo)) - 0.5), K, n - 1).astype(np.int64)
+    return (out * 0x9E3779B1 + 12345) & (n - 1)    # n is a power of two: an odd multiplier permutes ids
+
+
+def c5_block(b: int, seed: int = SEED_BASE + 4, spec: GraphSpec = C5):
+    """Events of session block b: (t, session id, event index, src, dst),
+    unsorted, t relative to the span start."""
+    rng = np.random.default_rng([seed, b])
+    S_total = int(math.ceil(spec.m / spec.mu))
+    S = (S_total + C5_BLOCKS - 1) // C5_BLOCKS
+    lo = b * spec.span // C5_BLOCKS
+    hi = (b + 1) * spec.span // C5_BLOCKS
+    u = _capped_zipf(rng, S, spec.n, spec.alpha, spec.cap)
+    v = _capped_zipf(rng, S, spec.n, spec.alpha, spec.cap)
+    clash = u == v
+    v[clash] = (u[clash] + 1) & (spec.n - 1)
+    selfl = rng.random(S) < spec.p_self
+    v[selfl] = u[selfl]
+    start = rng.integers(lo, hi, S, dtype=np.int64)
+    k = np.minimum(rng.geometric(1.0 / spec.mu, S), C5_MAX_EVENTS).astype(np.int64)
+    total = int(k.sum())
+    sess = np.repeat(np.arange(S, dtype=np.int64), k)
+    ev = np.arange(total, dtype=np.int64) - np.repeat(np.cumsum(k) - k, k)
+    gap = rng.exponential(spec.beta, total)
+    gap[ev == 0] = 0.0
+    cg = np.cumsum(gap)
+    off = np.floor(cg - np.repeat(cg[np.cumsum(k) - k], k)).astype(np.int64)
+    t = start[sess] + off
+    es, ed = u[sess], v[sess]
+    rev = rng.random(total) < spec.p_reply
+    es, ed = np.where(rev, ed, es), np.where(rev, es, ed)
+    keep = (off <= C5_MAX_SESSION) & (t < spec.span)
+    return t[keep], sess[keep] + b * S, ev[keep], es[keep], ed[keep]
+
+
+def c5_slice(ta: int, tb: int, seed: int = SEED_BASE + 4, spec: GraphSpec = C5):
+    """The C5 events with ta <= t < tb (relative seconds), ordered by
+    (t, session, event): (src u32, dst u32, t i64 (absolute), n)."""
+    b0 = max(0, (ta - C5_MAX_SESSION) * C5_BLOCKS // spec.span - 1)
+    b1 = min(C5_BLOCKS, tb * C5_BLOCKS // spec.span + 1)
+    keys, es, ds = [], [], []
+    for b in range(b0, b1):
+        t, sess, ev, s, d = c5_block(b, seed, spec)
+        k = (t >= ta) & (t < tb)
+        # (t, session, event) in one int64: t < 2^27 s, session < 2^30, event < 2^6
+        keys.append((t[k] << 36) | (sess[k] << 6) | ev[k]); es.append(s[k].astype(np.uint32))
+        ds.append(d[k].astype(np.uint32))
+    key = np.concatenate(keys)
+    o = np.argsort(key)
+    return np.concatenate(es)[o], np.concatenate(ds)[o], (key[o] >> 36) + spec.t0, spec.n
+
+
+def c5_rank_slice(rank: int, world: int, delta: int, seed: int = SEED_BASE + 4, spec: GraphSpec = C5):
+    """Rank `rank` of `world`'s share of C5: the roots with t in an equal
+    time range plus the forward δ-halo.  Returns (src, dst, t,
+    n, n_roots): edges [0, n_roots) are the rank's roots."""
+    ta = rank * spec.span // world
+    tb = (rank + 1) * spec.span // world
+    src, dst, t, n = c5_slice(ta, min(spec.span, tb + delta + 1), seed, spec)
+    n_roots = int(np.searchsorted(t, tb + spec.t0, side="left"))
+    return src, dst, t, n, n_roots

@@ -275,3 +275,30 @@ def test_validation():
         oracle.Graph(np.array([0], np.uint32), np.array([5], np.uint32), np.array([0], np.int64), 2)
     e = oracle.Graph(np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.int64), 3)
     assert e.mine(M.TRI, 10)["count"] == 0   # empty graph is valid
+
+
+def test_c5_slices_agree_and_tile():
+    """The C5 time-slice generator (input infrastructure): overlapping slices
+    agree on their shared events, adjacent rank slices tile the roots, and
+    each rank's halo is exactly the next rank's first δ-window."""
+    from paper_2310_02800_b200 import synth
+    import dataclasses
+    spec = dataclasses.replace(synth.C5, m=20_000_000, span=synth.C5.span)   # same shape, 1 % of the events
+    day = 86400
+    a = synth.c5_slice(5 * day, 8 * day, spec=spec)
+    b = synth.c5_slice(6 * day, 9 * day, spec=spec)
+    lo, hi = 6 * day + spec.t0, 8 * day + spec.t0
+    ka, kb = (a[2] >= lo), (b[2] < hi)
+    assert ka.sum() > 1000
+    for x, y in zip(a[:3], b[:3]):
+        assert np.array_equal(x[ka], y[kb])
+    assert np.all(np.diff(a[2]) >= 0)
+    w = 4000
+    r0 = synth.c5_rank_slice(0, w, 3600, spec=spec)
+    r1 = synth.c5_rank_slice(1, w, 3600, spec=spec)
+    n0 = r0[4]
+    halo = r0[2][n0:]
+    tb = spec.span // w + spec.t0                   # the rank boundary
+    assert np.all(r0[2][:n0] < tb) and np.all(r1[2] >= tb)
+    assert len(halo) == np.searchsorted(r1[2], tb + 3600, "right")   # exactly the next δ-window
+    assert np.array_equal(r0[0][n0:], r1[0][:len(halo)])
