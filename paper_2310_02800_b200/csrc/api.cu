@@ -17,6 +17,7 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
                        const tm_graph_opts *o, tm_graph **out);
 void graph_destroy(tm_graph *g);
 cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, uint64_t *scratch, cudaStream_t s);
+cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s);
 size_t horizon_scratch_words(uint64_t m);
 
 namespace {
@@ -152,10 +153,11 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     uint32_t *hbuf = nullptr;
     TM_CUDA_TRY(dev_alloc((void **)&scratch, kScratchWords * sizeof(unsigned long long), s));
     struct Free {
-        void *a, *b, *c, *d;
+        void *a, *b, *c, *d, *e;
         cudaStream_t s;
-        ~Free() { dev_free(a, s); dev_free(b, s); dev_free(c, s); dev_free(d, s); }
-    } fr{scratch, nullptr, nullptr, nullptr, s};
+        ~Free() { dev_free(a, s); dev_free(b, s); dev_free(c, s); dev_free(d, s); dev_free(e, s); }
+    } fr{scratch, nullptr, nullptr, nullptr, nullptr, s};
+    uint32_t *hrbuf = nullptr;
     TM_CUDA_TRY(cudaMemsetAsync(scratch, 0, kScratchWords * sizeof(unsigned long long), s));
     uint64_t *hscr = nullptr;
     if (need_h) {
@@ -174,6 +176,38 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     if (need_h) {
         p.H = hbuf;
         for (uint32_t i = 0; i + 1 < mo->L; i++) p.Hf[i] = gap_buf[i] >= 0 ? hbuf + (size_t)gap_buf[i] * m : nullptr;
+        // window-end ranks (build_hrank) for the levels whose list is anchored at
+        // the previous edge and bounded by a gap horizon; one array per distinct
+        // (list variant, horizon).  The instrumentation run (kStats) does not use them.
+        if (TM_HRANK && mode != kStats) {
+            Shape sh{};
+            sh.L = (int)mo->L;
+            for (uint32_t i = 0; i < mo->L; i++) { sh.u[i] = mo->u[i]; sh.v[i] = mo->v[i]; }
+            std::vector<std::pair<int, int>> keys;   // (variant, horizon index)
+            int which[kMaxL];
+            for (int nl = 1; nl < sh.L; nl++) {
+                which[nl - 1] = -1;
+                if (gap_buf[nl - 1] < 0 || sh.pairk(nl) || sh.anc(nl) != nl - 1) continue;
+                const std::pair<int, int> k{sh.avar(nl), gap_buf[nl - 1]};
+                auto it = std::find(keys.begin(), keys.end(), k);
+                which[nl - 1] = (int)(it - keys.begin());
+                if (it == keys.end()) keys.push_back(k);
+            }
+            if (!keys.empty()) {
+                TM_CUDA_TRY(dev_alloc((void **)&hrbuf, keys.size() * m * sizeof(uint32_t), s));
+                fr.e = hrbuf;
+                if (TM_HRANK == 2) {   // memo: 0 = not yet known
+                    TM_CUDA_TRY(cudaMemsetAsync(hrbuf, 0, keys.size() * m * sizeof(uint32_t), s));
+                } else {
+                    for (size_t i = 0; i < keys.size(); i++) {
+                        TM_CUDA_TRY(build_hrank(d, keys[i].first, hbuf + (size_t)keys[i].second * m, hrbuf + i * m, s));
+                        g_info.launches++;
+                    }
+                }
+                for (int nl = 1; nl < sh.L; nl++)
+                    p.HR[nl - 1] = which[nl - 1] >= 0 ? hrbuf + (size_t)which[nl - 1] * m : nullptr;
+            }
+        }
     }
     TM_CUDA_TRY(cudaEventRecord(ev[1], s));
 

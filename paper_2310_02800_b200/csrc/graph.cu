@@ -351,6 +351,83 @@ cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, uint
     return cudaGetLastError();
 }
 
+namespace {
+// Window-end ranks of one horizon: R[e] = the position of the
+// first record in list `var` of edge e (0 OUT(src e), 1 IN(src e), 2 OUT(dst
+// e), 3 IN(dst e)) whose edge id exceeds H[e] — i.e. the end of the
+// candidate window (e, H[e]] in that list.  A search node whose list is
+// anchored at its own last edge e_prev and whose tighter bound is the gap
+// horizon H_δi[e_prev] then knows its window end from one load; computed once
+// per edge and query instead of once per search node (on C4 every edge is
+// e_prev of ~11 nodes).  Gallop from the window start rank[var][e]: windows
+// are δ-short and every list ends in an id-0xFFFFFFFF sentinel.
+// window end of edge e when it lies beyond the first sector: gallop from
+// a (the first unread position), capped at the list's sentinel
+__device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ vtx,
+                                            const uint32_t *__restrict__ offs, uint64_t e, uint32_t a, uint32_t lim) {
+    const uint32_t last = __ldg(offs + vtx[e] + 1) - 1;
+    uint32_t lo = a, step = 4, hi = min(lo + 3, last);
+    while ((uint32_t)(__ldg(rec + hi) >> 32) <= lim) {
+        lo = hi + 1;
+        step <<= 1;
+        hi = min(lo + step - 1, last);
+    }
+    while (lo < hi) {   // first id > lim in [lo, hi]; rec[hi] qualifies
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        if ((uint32_t)(__ldg(rec + mid) >> 32) > lim) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+constexpr int kHrUnroll = 4;   // edges per thread in flight (independent load chains)
+
+__global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ rank,
+                                               const uint32_t *__restrict__ vtx, const uint32_t *__restrict__ offs,
+                                               const uint32_t *__restrict__ H, uint64_t m, uint32_t *__restrict__ R) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < m; e0 += stride * kHrUnroll) {
+        uint32_t lim[kHrUnroll], b[kHrUnroll];
+        ulonglong2 x0[kHrUnroll], x1[kHrUnroll];
+#pragma unroll
+        for (int u = 0; u < kHrUnroll; u++) {
+            const uint64_t e = e0 + u * stride;
+            lim[u] = e < m ? H[e] : 0u;
+            b[u] = e < m ? rank[e] : 0u;   // first record after e
+        }
+        // the aligned 32-byte sector (4 records) holding the window start:
+        // windows are δ_i-short, so it usually holds the end too
+#pragma unroll
+        for (int u = 0; u < kHrUnroll; u++) {
+            const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(rec + (b[u] & ~3u));
+            x0[u] = __ldg(v);
+            x1[u] = __ldg(v + 1);
+        }
+#pragma unroll
+        for (int u = 0; u < kHrUnroll; u++) {
+            const uint64_t e = e0 + u * stride;
+            if (e >= m) break;
+            const uint32_t a = b[u] & ~3u;
+            const uint32_t id[4] = {(uint32_t)(x0[u].x >> 32), (uint32_t)(x0[u].y >> 32), (uint32_t)(x1[u].x >> 32),
+                                    (uint32_t)(x1[u].y >> 32)};
+            uint32_t ans = 0xFFFFFFFFu;
+#pragma unroll
+            for (int k = 3; k >= 0; --k)
+                if (a + k >= b[u] && id[k] > lim[u]) ans = a + k;
+            if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, vtx, offs, e, a + 4, lim[u]);
+            R[e] = ans;
+        }
+    }
+}
+}  // namespace
+
+cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s) {
+    if (!d.m) return cudaSuccess;
+    k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, d.rank + (size_t)var * d.m, var < 2 ? d.src : d.dst,
+                                          (var & 1) ? d.off_in : d.off_out, H, d.m, R);
+    return cudaGetLastError();
+}
+
 tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m, uint32_t n,
                        const tm_graph_opts *o, tm_graph **out) {
     cudaStream_t s = o ? (cudaStream_t)o->stream : nullptr;

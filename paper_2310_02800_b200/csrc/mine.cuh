@@ -44,6 +44,10 @@ constexpr int kRootChunk = 128;      // roots claimed per global atomic
 #define TM_SHARE_MIN 128
 #endif
 constexpr int kShareMin = TM_SHARE_MIN;   // smallest window handed to an idle warp (share = 0)
+#ifndef TM_HRANK
+#define TM_HRANK 1          // window-end ranks: 0 off, 1 precomputed per query (build_hrank), 2 memoised in-kernel
+#endif
+constexpr bool kHrankMemo = TM_HRANK == 2;
 #ifndef TM_SHARE_POLL
 #define TM_SHARE_POLL 16
 #endif
@@ -489,7 +493,11 @@ struct Warp {
         if (ok) {
             const uint32_t *hf = p.Hf[NL - 1];
             uint32_t lim = hi;   // min(t_root + δ, t_prev + δ_i) as an id; H_δi read when needed
-            if (MODE == kStats || !plan.template pairk<NL>()) lim = hf ? min(hi, __ldg(hf + e)) : hi;
+            uint32_t hfv = ~0u;
+            if (MODE == kStats || !plan.template pairk<NL>()) {
+                if (hf) hfv = __ldg(hf + e);
+                lim = min(hi, hfv);
+            }
             if (MODE == kStats) {
                 // instrumentation of Algorithm 1 itself: shorter list (Q8), two binary searches
                 const int uM = plan.template u<NL>(), vM = plan.template v<NL>(), nb = plan.template nv<NL>();
@@ -542,8 +550,17 @@ struct Warp {
                 // runs past them is measured by a gallop.
                 const int dir = plan.template ldir<NL>(), var = plan.template avar<NL>(), j = plan.template anc<NL>();
                 const uint32_t ea = (j == NL - 1) ? e : pick(eh, j);
+                // window end from the horizon-rank array when the list is anchored
+                // at e itself and the gap bound H_δi[e] is the tighter one: one
+                // load, issued with the start and H_δi loads (no record reads)
+                uint32_t *hr = (j == NL - 1) ? p.HR[NL - 1] : nullptr;
+                uint32_t hrv = 0;
+                if (hr) hrv = kHrankMemo ? __ldcg(hr + e) : __ldg(hr + e);   // the memo is written by this kernel
                 lo = __ldg(p.rank + (size_t)var * p.m + ea);
                 if (j != NL - 1) lo = scan_after(p.rec, lo, e);
+                const bool fine_binds = hr && hfv <= hi;            // lim == H_δi[e]: the end depends on e only
+                const bool known = fine_binds && (!kHrankMemo || hrv != 0);
+                const uint32_t up_known = kHrankMemo ? hrv - 1 : hrv;
                 uint32_t pp = lo;
                 bool done = false;
                 uint32_t cnt = 0;
@@ -551,7 +568,8 @@ struct Warp {
                 // leaf parent: the last motif edge's window is scanned in this
                 // lane and its matches counted (or emitted) on the spot, for up
                 // to kLeafSectors sectors; non-leaf: one sector to size the window
-                const int nsec = leaf ? kLeafSectors : 1;
+                // (none when the end is known)
+                const int nsec = leaf ? kLeafSectors : (known ? 0 : 1);
 #pragma unroll 1
                 for (int it = 0; it < nsec && !done; ++it) {
                     const uint32_t a4 = pp & ~3u;
@@ -575,17 +593,22 @@ struct Warp {
                     leaf_count += cnt;
                     if (MODE == kRoots && cnt) atomicAdd(&p.root_counts[rslot], (unsigned long long)cnt);
                 }
-                if (leaf && done) {
-                    lo = up = 0;                            // fully scanned
-                } else if (!done) {
+                if (!done) {
                     // exact end: gallop from the first unread sector, bounded by the list's
                     // sentinel (an open-ended task scanned by the warp measured slower:
                     // it cannot share a batch with other tasks)
                     lo = leaf ? pp : lo;                    // a leaf keeps only its unscanned remainder
-                    const uint32_t x = pick(phi, plan.template lx<NL>());
-                    const uint32_t en = __ldg((dir == 0 ? p.off_out : p.off_in) + x + 1) - 1;
-                    up = gallop_after(p.rec, pp, en, lim);
+                    if (known) {
+                        up = up_known;
+                    } else {
+                        const uint32_t x = pick(phi, plan.template lx<NL>());
+                        const uint32_t en = __ldg((dir == 0 ? p.off_out : p.off_in) + x + 1) - 1;
+                        up = gallop_after(p.rec, pp, en, lim);
+                    }
                 }
+                // first visit of e at this level: remember its window end (pos + 1)
+                if (kHrankMemo && fine_binds && !known) __stcg(hr + e, up + 1);
+                if (leaf && done) lo = up = 0;              // fully scanned
             }
         }
         const bool keep = ok && up > lo;

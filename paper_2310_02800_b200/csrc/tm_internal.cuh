@@ -147,6 +147,9 @@ struct MineParams {
     uint32_t fmask;
     const uint32_t *H;                 // H_δ  (coarse δ-horizon)
     const uint32_t *Hf[kMaxL];         // H_{δ_i} per gap i, nullptr when δ_i = ∞
+    uint32_t *HR[kMaxL];               // per gap i: window-end ranks of H_{δ_i} in the list motif edge
+                                       // i+1 reads (build_hrank, or a zeroed memo of pos + 1 the kernel
+                                       // fills, TM_HRANK == 2), nullptr when not applicable
     uint64_t root_lo, n_roots;         // roots root_lo + [0, n_roots) ...
     const uint64_t *roots;             // ... or roots[0, n_roots) when non-null
     unsigned long long *scratch;       // [0] root cursor, [1] count, [2] enum cursor, [8..] stats
