@@ -106,26 +106,38 @@ class ClockSampler:
         self.lines = []
         self.p = None
 
-    def __enter__(self):
+    def resume(self):
+        """Start sampling (the timed steps); pause() stops it for the untimed
+        work in between (graph builds, the e2e pass: nvidia-smi's driver
+        queries slow host-synchronous API sequences down)."""
+        if self.p:
+            return
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                       "-lms", "50", "-i", str(self.index)], stdout=subprocess.PIPE,
                                       stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t = threading.Thread(target=self._read, args=(self.p,), daemon=True)
             self.t.start()
         except OSError:
             self.p = None
-        return self
 
-    def _read(self):
-        for line in self.p.stdout:
-            self.lines.append(line.strip())
-
-    def __exit__(self, *a):
+    def pause(self):
         if self.p:
             time.sleep(0.25)
             self.p.terminate()
             self.p.wait()
+            self.t.join(timeout=1.0)
+            self.p = None
+
+    def __enter__(self):
+        return self
+
+    def _read(self, proc):
+        for line in proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        self.pause()
 
     def summary(self):
         sm, mx, reasons, under = [], 0.0, set(), []
@@ -240,6 +252,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C4")
+    ap.add_argument("--separate", action="store_true",
+                    help="one tm_count per motif instead of one tm_count_multi query (A/B)")
     args = ap.parse_args()
     select_config(args.config)
 
@@ -289,15 +303,22 @@ def main():
     balance = [None] * len(MOTIFS)   # load balance of the last step's mining kernels (§8 a8)
 
     def step(g, rr):
-        cs, mine, launches = [], [], 0
-        for i, mo in enumerate(motifs):
-            cs.append(T.tm_count(g, mo, root_range=rr, stream=stream))
-            info = T.tm_last_run_info()
-            mine.append(info["mine_ms"])
-            launches += info["launches"]
-            balance[i] = {"shared_tasks": info["shared_tasks"], "tail_ms": info["tail_ms"],
-                          "warp_busy": info["warp_busy"]}
-        return cs, mine, launches
+        if args.separate:   # one tm_count per motif, each building its own horizons
+            cs, mine, launches = [], [], 0
+            for i, mo in enumerate(motifs):
+                cs.append(T.tm_count(g, mo, root_range=rr, stream=stream))
+                info = T.tm_last_run_info()
+                mine.append(info["mine_ms"])
+                launches += info["launches"]
+                balance[i] = {"shared_tasks": info["shared_tasks"], "tail_ms": info["tail_ms"],
+                              "warp_busy": info["warp_busy"]}
+            return cs, mine, launches
+        # one query for all motifs: the horizons / window-end ranks they share are built once
+        cs = T.tm_count_multi(g, motifs, root_range=rr, stream=stream)
+        kin = T.tm_last_kernel_info()
+        for i, x in enumerate(kin):
+            balance[i] = {"shared_tasks": x["shared_tasks"], "tail_ms": x["tail_ms"], "warp_busy": x["warp_busy"]}
+        return cs, [x["mine_ms"] for x in kin], T.tm_last_run_info()["launches"]
 
     def timed(fn):
         with torch.cuda.stream(stream):
@@ -323,6 +344,7 @@ def main():
             if world > 1 and (CONFIG != "C5" or C5_PARTS % world == 0):   # same part count on every rank
                 dist.barrier()
             torch.cuda.synchronize()
+            clk.resume()
             for k in range(args.steps):
                 ms, (cs, mm, nl) = timed(lambda: step(g, rr))
                 step_ms[k] += ms
@@ -330,6 +352,7 @@ def main():
                 if k == 0:
                     mine_ms += np.array(mm)
                     counts += np.array(cs, np.int64)
+            clk.pause()
             my_roots += rr[1] - rr[0]
             if pi == 0:   # roofline inputs (untimed instrumentation runs) from this rank's first part
                 stats = [T.tm_search_stats_run(g, mo, root_range=rr, stream=stream) for mo in motifs]
@@ -347,7 +370,8 @@ def main():
 
                 def e2e_step():
                     gg = T.Graph(hs, hd, ht, n, device=local, stream=stream)
-                    cs = [T.tm_count(gg, mo, root_range=rr, stream=stream) for mo in motifs]
+                    cs = ([T.tm_count(gg, mo, root_range=rr, stream=stream) for mo in motifs] if args.separate
+                  else T.tm_count_multi(gg, motifs, root_range=rr, stream=stream))
                     gg.close()
                     return cs
 
@@ -422,7 +446,10 @@ def main():
                 "matches_per_s": matches_per_s, "counts": dict(zip(MOTIFS, counts)),
                 "hbm_pct_of_peak": roofline["frac"] * 100, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk.summary(), "gpu_launches": int(launches) * world,
-                "gpu_launches_note": "per rank: H_δ (+ H_δi) horizon kernels and one mining kernel per query"}
+                "gpu_launches_note": "per rank and step: 2 kernels per distinct horizon, one window-end-rank kernel per "
+                                     "distinct (list, gap bound), one mining kernel per motif",
+                "query": "one tm_count per motif" if args.separate else
+                         "one tm_count_multi over the motifs (shared horizons and window-end ranks)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

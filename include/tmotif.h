@@ -179,6 +179,30 @@ typedef struct {
 tm_status tm_search_stats_run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *o,
                               tm_search_stats *out);
 
+/* Several motifs over the same root range in one query: counts[i] = the
+ * tm_count of mos[i].  The query-time structures — the δ-horizons of every
+ * distinct δ / δ_i and the window-end ranks of every
+ * distinct (list, gap bound) — are built once and shared, then one mining
+ * kernel per motif runs on o->stream.  mos: k host pointers; counts: host,
+ * k entries.  Synchronous.  Errors: as tm_count; TM_EINVAL for k == 0.
+ * tm_last_kernel_info reports each motif's kernel. */
+tm_status tm_count_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, const tm_run_opts *o,
+                         uint64_t *counts);
+
+/* Per mining kernel of the calling thread's last tm_count / tm_count_multi /
+ * tm_enumerate / tm_count_roots / tm_search_stats_run (one entry per motif):
+ * its CUDA-event time and load balance (fields as in tm_run_info). */
+typedef struct {
+    float mine_ms;
+    float tail_ms;
+    float warp_busy;
+    uint32_t grid_ctas;
+    uint64_t shared_tasks;
+} tm_kernel_info;
+
+/* Copies min(cap, n) entries to out (host); *n = number of kernels. */
+tm_status tm_last_kernel_info(tm_kernel_info *out, uint32_t cap, uint32_t *n);
+
 /* Fused census of the 36 two/three-node three-edge motifs (SURVEY.md §8(f)
  * N1, config C2): counts[a*6 + b] = the δ-temporal count of the
  * motif (0->1, E[a], E[b]), E = [0->1, 1->0, 0->2, 2->0, 1->2, 2->1], for the

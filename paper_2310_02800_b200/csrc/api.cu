@@ -2,6 +2,7 @@
 // canonicalisation, the per-query horizon construction and the mining
 // launch.  Every step of the hot path runs in this library's kernels.
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -92,11 +93,18 @@ struct RunOut {
     uint64_t stats[kScratchWords] = {};
 };
 
-// One query: horizons for δ and every effective δ_i, then the mining kernel.
-tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, int mode, uint32_t *enum_dev,
-              uint64_t cap, const uint64_t *roots_dev, uint64_t n_roots_list, unsigned long long *root_counts_dev,
-              RunOut *out) {
-    if (!g || !mo) return fail(TM_EINVAL, "null graph or motif");
+// One query over k motifs (k = 1: tm_count & co; k > 1: tm_count_multi):
+// the δ-horizons of every distinct δ / δ_i and the window-end ranks of every
+// distinct (list variant, gap horizon) are built once, then one mining kernel
+// per motif runs on the same stream.
+thread_local std::vector<tm_kernel_info> g_kinfo;
+
+tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, const tm_run_opts *opts, int mode,
+                    uint32_t *enum_dev, uint64_t cap, const uint64_t *roots_dev, uint64_t n_roots_list,
+                    unsigned long long *root_counts_dev, RunOut *out) {
+    if (!g || !mos || k == 0) return fail(TM_EINVAL, "null graph or motif");
+    for (uint32_t i = 0; i < k; i++)
+        if (!mos[i]) return fail(TM_EINVAL, "null motif");
     tm_run_opts o;
     tm_run_opts_default(&o);
     if (opts) o = *opts;
@@ -106,194 +114,237 @@ tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, in
     const DeviceGraph &d = g->d;
     const uint64_t m = d.m;
     g_info = tm_run_info{};
+    g_kinfo.assign(k, tm_kernel_info{});
+    if (o.edge_id_offset + m > (1ull << 32)) return fail(TM_EINVAL, "edge_id_offset + m exceeds 2^32");
 
-    MineParams p;
-    std::memset(&p, 0, sizeof p);
-    p.src = d.src; p.dst = d.dst; p.off_out = d.off_out; p.off_in = d.off_in; p.rec = d.rec; p.rank = d.rank;
-    p.m = (uint32_t)m;
-    p.split = (uint32_t)(m + d.n);
-    p.prec = d.prec; p.ptab = d.ptab; p.pmask = d.pmask; p.pbits = d.pbits; p.fmask = d.fmask;
-    p.L = mo->L;
-    for (uint32_t i = 0; i < mo->L; i++) { p.u[i] = mo->u[i]; p.v[i] = mo->v[i]; }
+    MineParams base;
+    std::memset(&base, 0, sizeof base);
+    base.src = d.src; base.dst = d.dst; base.off_out = d.off_out; base.off_in = d.off_in; base.rec = d.rec;
+    base.rank = d.rank;
+    base.m = (uint32_t)m;
+    base.split = (uint32_t)(m + d.n);
+    base.prec = d.prec; base.ptab = d.ptab; base.pmask = d.pmask; base.pbits = d.pbits; base.fmask = d.fmask;
     if (roots_dev) {
-        p.roots = roots_dev;
-        p.n_roots = n_roots_list;
+        base.roots = roots_dev;
+        base.n_roots = n_roots_list;
     } else {
         uint64_t hi = std::min<uint64_t>(o.root_hi, m), lo = std::min<uint64_t>(o.root_lo, hi);
-        p.root_lo = lo;
-        p.n_roots = hi - lo;
+        base.root_lo = lo;
+        base.n_roots = hi - lo;
     }
-    if (o.edge_id_offset + m > (1ull << 32)) return fail(TM_EINVAL, "edge_id_offset + m exceeds 2^32");
-    p.id_offset = (uint32_t)o.edge_id_offset;
-    p.enum_buf = enum_dev;
-    p.cap = cap;
-    p.root_counts = root_counts_dev;
+    base.id_offset = (uint32_t)o.edge_id_offset;
+    base.enum_buf = enum_dev;
+    base.cap = cap;
+    base.root_counts = root_counts_dev;
+    base.share = o.share;
 
-    cudaEvent_t ev[4] = {};
-    for (auto &e : ev) TM_CUDA_TRY(cudaEventCreate(&e));
-    struct EvFree { cudaEvent_t *e; ~EvFree() { for (int i = 0; i < 4; i++) if (e[i]) cudaEventDestroy(e[i]); } } evf{ev};
-
-    // distinct horizons: H_δ, and H_{δ_i} for every finite δ_i < δ (a gap
-    // bound >= δ can never bind: t_prev >= t_root).
+    // distinct horizons over all motifs: each δ, and every finite δ_i < δ (a
+    // gap bound >= δ can never bind: t_prev >= t_root)
     std::vector<int64_t> hv;
-    const bool need_h = mo->L >= 2 && p.n_roots > 0;
-    int gap_buf[kMaxL];
-    if (need_h) {
-        hv.push_back(mo->delta);
-        for (uint32_t i = 0; i + 1 < mo->L; i++) {
-            gap_buf[i] = -1;
-            int64_t f = mo->fine[i];
+    auto hidx = [&](int64_t x) {
+        auto it = std::find(hv.begin(), hv.end(), x);
+        if (it != hv.end()) return (int)(it - hv.begin());
+        hv.push_back(x);
+        return (int)hv.size() - 1;
+    };
+    std::vector<int> dl(k, -1);
+    std::vector<std::array<int, kMaxL>> gap(k);
+    std::vector<std::pair<int, int>> hkeys;   // window-end ranks: (list variant, horizon index)
+    std::vector<std::array<int, kMaxL>> hwhich(k);
+    for (uint32_t i = 0; i < k; i++) {
+        const tm_motif *mo = mos[i];
+        gap[i].fill(-1);
+        hwhich[i].fill(-1);
+        if (mo->L < 2 || base.n_roots == 0) continue;
+        dl[i] = hidx(mo->delta);
+        for (uint32_t j = 0; j + 1 < mo->L; j++) {
+            const int64_t f = mo->fine[j];
             if (f == TM_DELTA_INF || f >= mo->delta) continue;
-            auto it = std::find(hv.begin(), hv.end(), f);
-            gap_buf[i] = (int)(it - hv.begin());
-            if (it == hv.end()) hv.push_back(f);
+            gap[i][j] = hidx(f);
+        }
+        // window-end ranks (build_hrank) for the levels whose list is anchored at
+        // the previous edge and bounded by a gap horizon.  The instrumentation
+        // run (kStats) does not use them.
+        if (!TM_HRANK || mode == kStats) continue;
+        Shape sh{};
+        sh.L = (int)mo->L;
+        for (uint32_t j = 0; j < mo->L; j++) { sh.u[j] = mo->u[j]; sh.v[j] = mo->v[j]; }
+        for (int nl = 1; nl < sh.L; nl++) {
+            if (gap[i][nl - 1] < 0 || sh.pairk(nl) || sh.anc(nl) != nl - 1) continue;
+            const std::pair<int, int> key{sh.avar(nl), gap[i][nl - 1]};
+            auto it = std::find(hkeys.begin(), hkeys.end(), key);
+            hwhich[i][nl - 1] = (int)(it - hkeys.begin());
+            if (it == hkeys.end()) hkeys.push_back(key);
         }
     }
-    unsigned long long *scratch = nullptr;
-    uint32_t *hbuf = nullptr;
-    TM_CUDA_TRY(dev_alloc((void **)&scratch, kScratchWords * sizeof(unsigned long long), s));
-    struct Free {
-        void *a, *b, *c, *d, *e;
-        cudaStream_t s;
-        ~Free() { dev_free(a, s); dev_free(b, s); dev_free(c, s); dev_free(d, s); dev_free(e, s); }
-    } fr{scratch, nullptr, nullptr, nullptr, nullptr, s};
-    uint32_t *hrbuf = nullptr;
-    TM_CUDA_TRY(cudaMemsetAsync(scratch, 0, kScratchWords * sizeof(unsigned long long), s));
-    uint64_t *hscr = nullptr;
-    if (need_h) {
-        TM_CUDA_TRY(dev_alloc((void **)&hbuf, hv.size() * m * sizeof(uint32_t), s));
-        fr.b = hbuf;
-        TM_CUDA_TRY(dev_alloc((void **)&hscr, horizon_scratch_words(m) * sizeof(uint64_t), s));
-        fr.c = hscr;
-    }
-    p.scratch = scratch;
 
-    TM_CUDA_TRY(cudaEventRecord(ev[0], s));
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evd = nullptr;
+    std::vector<cudaEvent_t> evk(k, nullptr);
+    struct EvFree {
+        std::vector<cudaEvent_t *> e;
+        ~EvFree() { for (auto *p : e) if (*p) cudaEventDestroy(*p); }
+    } evf;
+    for (cudaEvent_t *e : {&ev0, &ev1, &evd}) { TM_CUDA_TRY(cudaEventCreate(e)); evf.e.push_back(e); }
+    for (auto &e : evk) { TM_CUDA_TRY(cudaEventCreate(&e)); evf.e.push_back(&e); }
+
+    struct Free {
+        std::vector<void *> v;
+        cudaStream_t s;
+        ~Free() { for (void *p : v) dev_free(p, s); }
+    } fr{{}, s};
+    unsigned long long *scratch = nullptr;
+    TM_CUDA_TRY(dev_alloc((void **)&scratch, (size_t)k * kScratchWords * sizeof(unsigned long long), s));
+    fr.v.push_back(scratch);
+    TM_CUDA_TRY(cudaMemsetAsync(scratch, 0, (size_t)k * kScratchWords * sizeof(unsigned long long), s));
+    uint32_t *hbuf = nullptr, *hrbuf = nullptr;
+    uint64_t *hscr = nullptr;
+    if (!hv.empty()) {
+        TM_CUDA_TRY(dev_alloc((void **)&hbuf, hv.size() * m * sizeof(uint32_t), s));
+        fr.v.push_back(hbuf);
+        TM_CUDA_TRY(dev_alloc((void **)&hscr, horizon_scratch_words(m) * sizeof(uint64_t), s));
+        fr.v.push_back(hscr);
+    }
+    if (!hkeys.empty()) {
+        TM_CUDA_TRY(dev_alloc((void **)&hrbuf, hkeys.size() * m * sizeof(uint32_t), s));
+        fr.v.push_back(hrbuf);
+    }
+
+    TM_CUDA_TRY(cudaEventRecord(ev0, s));
     for (size_t i = 0; i < hv.size(); i++) {
         TM_CUDA_TRY(build_horizon(d, hv[i], hbuf + i * m, hscr, s));
         g_info.launches += 2;
     }
-    if (need_h) {
-        p.H = hbuf;
-        for (uint32_t i = 0; i + 1 < mo->L; i++) p.Hf[i] = gap_buf[i] >= 0 ? hbuf + (size_t)gap_buf[i] * m : nullptr;
-        // window-end ranks (build_hrank) for the levels whose list is anchored at
-        // the previous edge and bounded by a gap horizon; one array per distinct
-        // (list variant, horizon).  The instrumentation run (kStats) does not use them.
-        if (TM_HRANK && mode != kStats) {
-            Shape sh{};
-            sh.L = (int)mo->L;
-            for (uint32_t i = 0; i < mo->L; i++) { sh.u[i] = mo->u[i]; sh.v[i] = mo->v[i]; }
-            std::vector<std::pair<int, int>> keys;   // (variant, horizon index)
-            int which[kMaxL];
-            for (int nl = 1; nl < sh.L; nl++) {
-                which[nl - 1] = -1;
-                if (gap_buf[nl - 1] < 0 || sh.pairk(nl) || sh.anc(nl) != nl - 1) continue;
-                const std::pair<int, int> k{sh.avar(nl), gap_buf[nl - 1]};
-                auto it = std::find(keys.begin(), keys.end(), k);
-                which[nl - 1] = (int)(it - keys.begin());
-                if (it == keys.end()) keys.push_back(k);
-            }
-            if (!keys.empty()) {
-                TM_CUDA_TRY(dev_alloc((void **)&hrbuf, keys.size() * m * sizeof(uint32_t), s));
-                fr.e = hrbuf;
-                if (TM_HRANK == 2) {   // memo: 0 = not yet known
-                    TM_CUDA_TRY(cudaMemsetAsync(hrbuf, 0, keys.size() * m * sizeof(uint32_t), s));
-                } else {
-                    for (size_t i = 0; i < keys.size(); i++) {
-                        TM_CUDA_TRY(build_hrank(d, keys[i].first, hbuf + (size_t)keys[i].second * m, hrbuf + i * m, s));
-                        g_info.launches++;
-                    }
-                }
-                for (int nl = 1; nl < sh.L; nl++)
-                    p.HR[nl - 1] = which[nl - 1] >= 0 ? hrbuf + (size_t)which[nl - 1] * m : nullptr;
+    if (!hkeys.empty()) {
+        if (TM_HRANK == 2) {   // memo: 0 = not yet known
+            TM_CUDA_TRY(cudaMemsetAsync(hrbuf, 0, hkeys.size() * m * sizeof(uint32_t), s));
+        } else {
+            for (size_t i = 0; i < hkeys.size(); i++) {
+                TM_CUDA_TRY(build_hrank(d, hkeys[i].first, hbuf + (size_t)hkeys[i].second * m, hrbuf + i * m, s));
+                g_info.launches++;
             }
         }
     }
-    TM_CUDA_TRY(cudaEventRecord(ev[1], s));
+    TM_CUDA_TRY(cudaEventRecord(ev1, s));
 
-    if (p.n_roots > 0) {
-        bool spec = false;
-        KernelInfo ki = lookup_kernel(mo->code, mode, &spec);
-        const int threads = kWarpsPerBlock * 32;
-        const size_t smem = (size_t)ki.smem_per_warp * kWarpsPerBlock;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        {
-            std::lock_guard<std::mutex> lk(g_attr_mu);
-            auto key = (const void *)ki.fn;
-            if (!g_attr_done.count(key)) {
-                TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-#ifdef TM_CARVEOUT_MAX
-                TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                                 (int)cudaSharedmemCarveoutMaxShared));
-#endif
-                g_attr_done[key] = 1;
+    void *qbuf = nullptr;   // heavy-subtree sharing queue, reused by the launches (stream order)
+    uint32_t qcap = 0;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    TM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int threads = kWarpsPerBlock * 32;
+    for (uint32_t i = 0; i < k; i++) {
+        const tm_motif *mo = mos[i];
+        MineParams p = base;
+        p.L = mo->L;
+        for (uint32_t j = 0; j < mo->L; j++) { p.u[j] = mo->u[j]; p.v[j] = mo->v[j]; }
+        p.scratch = scratch + (size_t)i * kScratchWords;
+        if (dl[i] >= 0) {
+            p.H = hbuf + (size_t)dl[i] * m;
+            for (uint32_t j = 0; j + 1 < mo->L; j++) {
+                p.Hf[j] = gap[i][j] >= 0 ? hbuf + (size_t)gap[i][j] * m : nullptr;
+                p.HR[j] = hwhich[i][j] >= 0 ? hrbuf + (size_t)hwhich[i][j] * m : nullptr;
             }
         }
-        int sms = 0, per_sm = 0;
-        TM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        TM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ki.fn, threads, smem));
-        if (per_sm < 1) return fail(TM_ECUDA, "mining kernel does not fit on an SM");
-        uint64_t grid = o.grid_ctas ? o.grid_ctas : (uint64_t)sms * per_sm;
-        // no more warps than 32-root batches
-        uint64_t max_useful = (p.n_roots + 31) / 32;
-        max_useful = (max_useful + kWarpsPerBlock - 1) / kWarpsPerBlock;
-        grid = std::max<uint64_t>(1, std::min(grid, max_useful));
-        // heavy-subtree sharing: idle warps wait for work, so every CTA must
-        // be resident at once (a CTA waiting for a slot would never start)
-        p.share = o.share;
-        if (p.share != 1) {
-            grid = std::min<uint64_t>(grid, (uint64_t)sms * per_sm);
-            p.total_warps = (uint32_t)(grid * kWarpsPerBlock);
-            uint32_t q = 32;
-            while (q < p.total_warps) q <<= 1;
-            p.qmask = q - 1;
-            void *qb = nullptr;
-            TM_CUDA_TRY(dev_alloc(&qb, (size_t)q * (sizeof(unsigned) + kShareWords * sizeof(uint32_t)), s));
-            fr.d = qb;
-            p.qflag = (unsigned *)qb;
-            p.qrec = (uint32_t *)((char *)qb + (size_t)q * sizeof(unsigned));
-            TM_CUDA_TRY(cudaMemsetAsync(p.qflag, 0, (size_t)q * sizeof(unsigned), s));
-        }
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)grid);
-        cfg.blockDim = dim3(threads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cfg.numAttrs = 0;
-        TM_CUDA_TRY(cudaLaunchKernelEx(&cfg, ki.fn, p));
-        g_info.launches++;
-        g_info.grid_ctas = (uint32_t)grid;
-        g_info.block_threads = threads;
-    }
-    TM_CUDA_TRY(cudaEventRecord(ev[2], s));
-    unsigned long long host[kScratchWords];
-    TM_CUDA_TRY(cudaMemcpyAsync(host, scratch, sizeof host, cudaMemcpyDeviceToHost, s));
-    TM_CUDA_TRY(cudaEventRecord(ev[3], s));
-    TM_CUDA_TRY(cudaStreamSynchronize(s));
-    cudaEventElapsedTime(&g_info.horizon_ms, ev[0], ev[1]);
-    cudaEventElapsedTime(&g_info.mine_ms, ev[1], ev[2]);
-    cudaEventElapsedTime(&g_info.total_ms, ev[0], ev[3]);
-    out->count = mode == kEnum ? host[2] : host[1];
-    g_info.shared_tasks = host[kShareDone];
-    if (host[kTimeStart] && host[kTimeExit]) {
-        const unsigned long long t0 = ~host[kTimeStart], te = host[kTimeExit];
-        const unsigned long long td = host[kTimeDrain] ? ~host[kTimeDrain] : te;
-        g_info.tail_ms = te > td ? (float)((te - td) * 1e-6) : 0.f;
-        if (te > t0 && g_info.grid_ctas)
-            g_info.warp_busy = (float)(((double)host[kTimeBusy] - (double)host[kTimeWait]) /
-                                       ((double)(te - t0) * g_info.grid_ctas * kWarpsPerBlock));
-    }
-#ifdef TM_PHASE_PROFILE
-    fprintf(stderr, "[phase]");
-    for (int l = 0; l < 6; l++)
-        if (host[21 + 2 * l])
-            fprintf(stderr, " L%d: steps=%llu cyc/step=%.0f share=%.3f", l, host[21 + 2 * l],
-                    (double)host[20 + 2 * l] / host[21 + 2 * l], 0.0 + host[20 + 2 * l]);
-    fprintf(stderr, "\n");
+        if (p.n_roots > 0) {
+            bool spec = false;
+            KernelInfo ki = lookup_kernel(mo->code, mode, &spec);
+            const size_t smem = (size_t)ki.smem_per_warp * kWarpsPerBlock;
+            {
+                std::lock_guard<std::mutex> lk(g_attr_mu);
+                auto key = (const void *)ki.fn;
+                if (!g_attr_done.count(key)) {
+                    TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+#ifdef TM_CARVEOUT_MAX
+                    TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                     (int)cudaSharedmemCarveoutMaxShared));
 #endif
-    for (int i = 0; i < kScratchWords; i++) out->stats[i] = host[i];
+                    g_attr_done[key] = 1;
+                }
+            }
+            int per_sm = 0;
+            TM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ki.fn, threads, smem));
+            if (per_sm < 1) return fail(TM_ECUDA, "mining kernel does not fit on an SM");
+            uint64_t grid = o.grid_ctas ? o.grid_ctas : (uint64_t)sms * per_sm;
+            // no more warps than 32-root batches
+            uint64_t max_useful = (p.n_roots + 31) / 32;
+            max_useful = (max_useful + kWarpsPerBlock - 1) / kWarpsPerBlock;
+            grid = std::max<uint64_t>(1, std::min(grid, max_useful));
+            // heavy-subtree sharing: idle warps wait for work, so every CTA must
+            // be resident at once (a CTA waiting for a slot would never start)
+            if (p.share != 1) {
+                grid = std::min<uint64_t>(grid, (uint64_t)sms * per_sm);
+                p.total_warps = (uint32_t)(grid * kWarpsPerBlock);
+                uint32_t q = 32;
+                while (q < p.total_warps) q <<= 1;
+                if (q > qcap) {
+                    if (qbuf) dev_free(qbuf, s);
+                    qbuf = nullptr;
+                    TM_CUDA_TRY(dev_alloc(&qbuf, (size_t)q * (sizeof(unsigned) + kShareWords * sizeof(uint32_t)), s));
+                    qcap = q;
+                }
+                p.qmask = q - 1;
+                p.qflag = (unsigned *)qbuf;
+                p.qrec = (uint32_t *)((char *)qbuf + (size_t)q * sizeof(unsigned));
+                TM_CUDA_TRY(cudaMemsetAsync(p.qflag, 0, (size_t)q * sizeof(unsigned), s));
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)grid);
+            cfg.blockDim = dim3(threads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cfg.numAttrs = 0;
+            TM_CUDA_TRY(cudaLaunchKernelEx(&cfg, ki.fn, p));
+            g_info.launches++;
+            g_info.grid_ctas = (uint32_t)grid;
+            g_info.block_threads = threads;
+            g_kinfo[i].grid_ctas = (uint32_t)grid;
+        }
+        TM_CUDA_TRY(cudaEventRecord(evk[i], s));
+    }
+    if (qbuf) fr.v.push_back(qbuf);
+    std::vector<unsigned long long> host((size_t)k * kScratchWords);
+    TM_CUDA_TRY(cudaMemcpyAsync(host.data(), scratch, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                s));
+    TM_CUDA_TRY(cudaEventRecord(evd, s));
+    TM_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaEventElapsedTime(&g_info.horizon_ms, ev0, ev1);
+    cudaEventElapsedTime(&g_info.mine_ms, ev1, evk[k - 1]);
+    cudaEventElapsedTime(&g_info.total_ms, ev0, evd);
+    for (uint32_t i = 0; i < k; i++) {
+        const unsigned long long *h = host.data() + (size_t)i * kScratchWords;
+        tm_kernel_info &ki = g_kinfo[i];
+        cudaEventElapsedTime(&ki.mine_ms, i ? evk[i - 1] : ev1, evk[i]);
+        ki.shared_tasks = h[kShareDone];
+        if (h[kTimeStart] && h[kTimeExit]) {
+            const unsigned long long t0 = ~h[kTimeStart], te = h[kTimeExit];
+            const unsigned long long td = h[kTimeDrain] ? ~h[kTimeDrain] : te;
+            ki.tail_ms = te > td ? (float)((te - td) * 1e-6) : 0.f;
+            if (te > t0 && ki.grid_ctas)
+                ki.warp_busy = (float)(((double)h[kTimeBusy] - (double)h[kTimeWait]) /
+                                       ((double)(te - t0) * ki.grid_ctas * kWarpsPerBlock));
+        }
+        out[i].count = mode == kEnum ? h[2] : h[1];
+        for (int w = 0; w < kScratchWords; w++) out[i].stats[w] = h[w];
+#ifdef TM_PHASE_PROFILE
+        fprintf(stderr, "[phase]");
+        for (int l = 0; l < 6; l++)
+            if (h[21 + 2 * l])
+                fprintf(stderr, " L%d: steps=%llu cyc/step=%.0f share=%.3f", l, h[21 + 2 * l],
+                        (double)h[20 + 2 * l] / h[21 + 2 * l], 0.0 + h[20 + 2 * l]);
+        fprintf(stderr, "\n");
+#endif
+    }
+    // the last motif's load balance in the single-query record
+    g_info.shared_tasks = g_kinfo[k - 1].shared_tasks;
+    g_info.tail_ms = g_kinfo[k - 1].tail_ms;
+    g_info.warp_busy = g_kinfo[k - 1].warp_busy;
     return TM_OK;
+}
+
+tm_status run(const tm_graph *g, const tm_motif *mo, const tm_run_opts *opts, int mode, uint32_t *enum_dev,
+              uint64_t cap, const uint64_t *roots_dev, uint64_t n_roots_list, unsigned long long *root_counts_dev,
+              RunOut *out) {
+    return run_multi(g, &mo, 1, opts, mode, enum_dev, cap, roots_dev, n_roots_list, root_counts_dev, out);
 }
 
 tm_status check_graph_args(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m, uint32_t n,
@@ -617,6 +668,24 @@ tm_status tm_census36(const tm_graph *g, int64_t delta, const int64_t *fine, con
     cudaEventElapsedTime(&g_info.mine_ms, ev[1], ev[2]);
     cudaEventElapsedTime(&g_info.total_ms, ev[0], ev[3]);
     for (int i = 0; i < 36; i++) counts[i] = host[i];
+    return TM_OK;
+}
+
+tm_status tm_count_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, const tm_run_opts *o,
+                         uint64_t *counts) {
+    g_err.clear();
+    if (!counts || !mos || k == 0) return fail(TM_EINVAL, "null argument or k == 0");
+    std::vector<RunOut> r(k);
+    tm_status st = run_multi(g, mos, k, o, kCount, nullptr, 0, nullptr, 0, nullptr, r.data());
+    if (st) return st;
+    for (uint32_t i = 0; i < k; i++) counts[i] = r[i].count;
+    return TM_OK;
+}
+
+tm_status tm_last_kernel_info(tm_kernel_info *out, uint32_t cap, uint32_t *n) {
+    if (!n || (cap && !out)) return fail(TM_EINVAL, "null argument");
+    *n = (uint32_t)g_kinfo.size();
+    for (uint32_t i = 0; i < cap && i < g_kinfo.size(); i++) out[i] = g_kinfo[i];
     return TM_OK;
 }
 

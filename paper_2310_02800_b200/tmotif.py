@@ -55,6 +55,11 @@ class RunInfo(ctypes.Structure):
                 ("tail_ms", _f32), ("warp_busy", _f32)]
 
 
+class KernelInfo(ctypes.Structure):
+    _fields_ = [("mine_ms", _f32), ("tail_ms", _f32), ("warp_busy", _f32), ("grid_ctas", _u32),
+                ("shared_tasks", _u64)]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -75,6 +80,8 @@ SIGNATURES = [
     ("tm_count_roots", _i32, [_P, _P, ctypes.POINTER(RunOpts), _P, _u64, _P]),
     ("tm_search_stats_run", _i32, [_P, _P, ctypes.POINTER(RunOpts), ctypes.POINTER(SearchStats)]),
     ("tm_census36", _i32, [_P, _i64, _P, ctypes.POINTER(RunOpts), _P]),
+    ("tm_count_multi", _i32, [_P, _P, _u32, ctypes.POINTER(RunOpts), _P]),
+    ("tm_last_kernel_info", _i32, [ctypes.POINTER(KernelInfo), _u32, ctypes.POINTER(_u32)]),
     ("tm_last_run_info", _i32, [ctypes.POINTER(RunInfo)]),
     ("tm_partition_plan", _i32, [_P, _u64, _i64, _u32, _P, _P, _P]),
     ("tm_last_error", ctypes.c_char_p, []),
@@ -279,6 +286,25 @@ def tm_search_stats_run(g: Graph, mo: Motif, **opts) -> dict:
     _check(lib().tm_search_stats_run(g.handle, mo.handle, ctypes.byref(o), ctypes.byref(s)))
     return {"nodes": list(s.nodes), "window_sum": s.window_sum, "list_sum": s.list_sum,
             "probe_sum": s.probe_sum, "matches": s.matches, "fast_window_sum": s.fast_window_sum}
+
+
+def tm_count_multi(g: Graph, motifs, **opts) -> list:
+    """Counts of several motifs in one query (shared horizons / window-end ranks)."""
+    k = len(motifs)
+    arr = (_P * k)(*[mo.handle for mo in motifs])
+    counts = np.zeros(k, np.uint64)
+    o = run_opts(**opts)
+    _check(lib().tm_count_multi(g.handle, arr, k, ctypes.byref(o), _host_ptr(counts)))
+    return [int(c) for c in counts]
+
+
+def tm_last_kernel_info() -> list:
+    n = _u32()
+    _check(lib().tm_last_kernel_info(None, 0, ctypes.byref(n)))
+    buf = (KernelInfo * max(1, n.value))()
+    _check(lib().tm_last_kernel_info(buf, n.value, ctypes.byref(n)))
+    return [{"mine_ms": b.mine_ms, "tail_ms": b.tail_ms, "warp_busy": b.warp_busy, "grid_ctas": b.grid_ctas,
+             "shared_tasks": b.shared_tasks} for b in buf[: n.value]]
 
 
 def tm_census36(g: Graph, delta: int, fine=None, **opts) -> np.ndarray:

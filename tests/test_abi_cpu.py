@@ -95,4 +95,5 @@ def test_declared_struct_sizes_match_binding():
     # 3 f32 + 3 u32, shared_tasks u64, tail_ms, warp_busy
     assert ctypes.sizeof(T.RunInfo) == 24 + 8 + 4 + 4
     assert T.RunInfo.shared_tasks.offset == 24
+    assert ctypes.sizeof(T.KernelInfo) == 24 and T.KernelInfo.shared_tasks.offset == 16
     assert ctypes.sizeof(T.SearchStats) == 8 * 13

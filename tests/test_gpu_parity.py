@@ -388,3 +388,36 @@ def test_census36_bursts_and_errors():
         T.tm_census36(g, -1)
     empty = T.Graph(np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.int64), 4)
     assert not T.tm_census36(empty, 10).any()
+
+
+# ------------------------------------------- several motifs in one query
+def test_count_multi_matches_single_queries_and_oracle():
+    """tm_count_multi shares the horizons and window-end ranks across motifs
+    with equal or different δ / δ_i; every count equals its own tm_count and
+    the oracle's."""
+    src, dst, t, n = synth.config_graph("C3", m=400_000)
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    specs = [("P3", 86400, [21600, 21600]), ("TRI", 86400, [21600, 21600]), ("C4", 86400, [21600] * 3),
+             ("DIA", 86400, [21600] * 4), ("TT", 3600, None), ("C4", 86400, [3600, None, 7200]),
+             ("TT2", 43200, [43200, 600, 100000])]
+    mos = [T.Motif(M.get(nm), d, f) for nm, d, f in specs]
+    got = T.tm_count_multi(g, mos)
+    info = T.tm_last_kernel_info()
+    assert len(info) == len(specs) and all(x["mine_ms"] >= 0 for x in info)
+    for (nm, d, f), mo, c in zip(specs, mos, got):
+        assert c == T.tm_count(g, mo) == og.mine(M.get(nm), d, f)["count"], (nm, d, f)
+    # root ranges and sharing modes pass through
+    half = len(src) // 2
+    assert T.tm_count_multi(g, mos, root_range=(half, len(src)), share=1) == \
+        [og.mine(M.get(nm), d, f, root_range=(half, len(src)))["count"] for nm, d, f in specs]
+    rng = random.Random(7)
+    for k in range(30):
+        s_, d_, t_, n_ = synth.tiny_graph(900 + k, n=rng.randint(2, 8), m=rng.randint(0, 80))
+        ms = [M.get(rng.choice(["P3", "TRI", "C4", "TT", "DIA", "PATH2"])) for _ in range(rng.randint(1, 4))]
+        dls = [rng.choice([0, 5, 20, INF]) for _ in ms]
+        fs = [None if rng.random() < 0.5 else random_fine(rng, len(mm)) for mm in ms]
+        gg = T.Graph(s_, d_, t_, n_)
+        oo = oracle.Graph(s_, d_, t_, n_)
+        res = T.tm_count_multi(gg, [T.Motif(mm, dd, ff) for mm, dd, ff in zip(ms, dls, fs)])
+        assert res == [oo.mine(mm, dd, ff)["count"] for mm, dd, ff in zip(ms, dls, fs)]

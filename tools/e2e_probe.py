@@ -32,3 +32,33 @@ for it in range(4):
     t3 = time.perf_counter()
     print(f"build {1e3 * (t1 - t0):.1f} ms  queries {1e3 * (t2 - t1):.1f} ms  destroy {1e3 * (t3 - t2):.1f} ms",
           file=sys.stderr)
+
+# the same through tm_count_multi, and a graph kept alive in between (as bench.py's timed part)
+keep = T.Graph(hs, hd, ht, n, stream=s)
+for it in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = T.Graph(hs, hd, ht, n, stream=s)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    T.tm_count_multi(g, mos, stream=s)
+    t2 = time.perf_counter()
+    g.close()
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    print(f"[multi, another graph resident] build {1e3 * (t1 - t0):.1f} ms  queries {1e3 * (t2 - t1):.1f} ms  "
+          f"destroy {1e3 * (t3 - t2):.1f} ms", file=sys.stderr)
+keep.close()
+for it in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = T.Graph(hs, hd, ht, n, stream=s)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    T.tm_count_multi(g, mos, stream=s)
+    t2 = time.perf_counter()
+    g.close()
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    print(f"[multi] build {1e3 * (t1 - t0):.1f} ms  queries {1e3 * (t2 - t1):.1f} ms  destroy {1e3 * (t3 - t2):.1f} ms",
+          file=sys.stderr)
