@@ -569,7 +569,9 @@ struct Warp {
                 // lane and its matches counted (or emitted) on the spot, for up
                 // to kLeafSectors sectors; non-leaf: one sector to size the window
                 // (none when the end is known)
-                const int nsec = leaf ? kLeafSectors : (known ? 0 : 1);
+                int nsec = leaf ? kLeafSectors : (known ? 0 : 1);
+                if (leaf && known)   // only the sectors the window covers; an empty window reads nothing
+                    nsec = up_known <= lo ? 0 : min(kLeafSectors, (int)(((up_known - 1) >> 2) - (lo >> 2)) + 1);
 #pragma unroll 1
                 for (int it = 0; it < nsec && !done; ++it) {
                     const uint32_t a4 = pp & ~3u;
