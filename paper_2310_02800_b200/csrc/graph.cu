@@ -492,7 +492,7 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     if (m) k_gather<<<grid_for(m), 256, 0, s>>>(d.perm, isrc, idst, it, m, d.src, d.dst, d.t);
     TRY(cudaGetLastError());
     TRY(build_csr(d, s));
-    TRY(build_pairs(d, s));
+    if (TM_PAIR_LEAF || TM_PAIR_NONLEAF) TRY(build_pairs(d, s));
     TRY(cudaStreamSynchronize(s));
 #undef TRY
     if (!on_dev) { dev_free(isrc, s); dev_free(idst, s); dev_free(it, s); }

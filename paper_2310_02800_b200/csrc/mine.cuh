@@ -57,12 +57,6 @@ constexpr unsigned kShareStop = 0xFFFFFFFFu;     // flag value: the search is co
 #define TM_SHARE_SLEEP 2048
 #endif
 constexpr unsigned kShareSleepMax = TM_SHARE_SLEEP;   // ns, longest back-off of a waiting warp
-#ifndef TM_PAIR_LEAF
-#define TM_PAIR_LEAF 0      // closing leaf edges read the pair index (measured: same time, 10x DRAM traffic)
-#endif
-#ifndef TM_PAIR_NONLEAF
-#define TM_PAIR_NONLEAF 1   // closing inner edges read the pair index
-#endif
 #ifndef TM_LEAF_SECTORS
 #define TM_LEAF_SECTORS 4
 #endif
