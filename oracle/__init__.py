@@ -26,6 +26,9 @@ _lib = None
 
 INF = (1 << 63) - 1  # δ = ∞
 MAXL = 8
+MAXV = 16
+MAXANTI = 4
+ANY = -1             # no label requirement
 
 OK, EINVAL, ENOMEM, EUNSUPPORTED = 0, 1, 2, 3
 _ERRS = {EINVAL: "invalid argument", ENOMEM: "out of memory", EUNSUPPORTED: "unsupported motif (prefix-disconnected, Q9)"}
@@ -46,6 +49,37 @@ class Stats(ctypes.Structure):
     def as_dict(self):
         return {"nodes": list(self.nodes), "window_sum": self.window_sum, "list_sum": self.list_sum,
                 "probe_sum": self.probe_sum, "matches": self.matches}
+
+
+class Constraints(ctypes.Structure):
+    """Labels / anti-edges of the generalized query (tmo_constraints)."""
+    _fields_ = [("vlabel", ctypes.c_int32 * MAXV), ("elabel", ctypes.c_int32 * MAXL), ("n_anti", ctypes.c_uint32),
+                ("anti_u", ctypes.c_uint32 * MAXANTI), ("anti_v", ctypes.c_uint32 * MAXANTI),
+                ("anti_attach", ctypes.c_uint32 * MAXANTI), ("anti_window", ctypes.c_int64 * MAXANTI)]
+
+
+def make_constraints(vlabels=None, elabels=None, anti=None):
+    """vlabels: {motif vertex: label}; elabels: per motif edge label or None;
+    anti: [(u, v, attach, window)] — attach = 0-based real motif edge."""
+    if not vlabels and not elabels and not anti:
+        return None
+    c = Constraints()
+    for i in range(MAXV):
+        c.vlabel[i] = ANY
+    for i in range(MAXL):
+        c.elabel[i] = ANY
+    for v, lab in (vlabels or {}).items():
+        c.vlabel[int(v)] = int(lab)
+    for i, lab in enumerate(elabels or []):
+        if lab is not None:
+            c.elabel[i] = int(lab)
+    anti = list(anti or [])
+    if len(anti) > MAXANTI:
+        raise ValueError("too many anti-edges")
+    c.n_anti = len(anti)
+    for j, (u, v, a, w) in enumerate(anti):
+        c.anti_u[j], c.anti_v[j], c.anti_attach[j], c.anti_window[j] = int(u), int(v), int(a), int(w)
+    return c
 
 
 def build(force: bool = False) -> str:
@@ -72,7 +106,9 @@ def _load():
             lib.tmo_graph_free.restype = None
             lib.tmo_graph_export.argtypes = [P, P, P, P, P]
             lib.tmo_graph_export.restype = None
-            lib.tmo_mine.argtypes = [P, u32, P, P, i64, P, u64, u64, P, u64, i32, P, P, P, u64, P, P]
+            lib.tmo_mine.argtypes = [P, u32, P, P, i64, P, P, u64, u64, P, u64, i32, P, P, P, u64, P, P]
+            lib.tmo_graph_set_labels.argtypes = [P, P, P]
+            lib.tmo_graph_set_labels.restype = i32
             lib.tmo_mine.restype = i32
             lib.tmo_max_threads.argtypes = []
             lib.tmo_max_threads.restype = i32
@@ -111,6 +147,17 @@ class Graph:
             _lib.tmo_graph_free(h)
             self._h = None
 
+    def set_labels(self, vlabels=None, elabels=None):
+        """Vertex labels (n) and edge labels (m, input order); None = all 0."""
+        va = None if vlabels is None else np.ascontiguousarray(vlabels, np.int32)
+        ea = None if elabels is None else np.ascontiguousarray(elabels, np.int32)
+        if va is not None and va.shape[0] != self.n or ea is not None and ea.shape[0] != self.m:
+            raise ValueError("label array length")
+        rc = _load().tmo_graph_set_labels(self._h, _ptr(va), _ptr(ea))
+        if rc:
+            raise OracleError(rc)
+        self._labels = (va, ea)
+
     def sorted_arrays(self):
         """(perm, src, dst, t) in sorted edge-id order; perm[id] = input position."""
         m = self.m
@@ -120,8 +167,12 @@ class Graph:
         return perm, s, d, t
 
     def mine(self, motif, delta: int, fine=None, *, root_range=None, roots=None, threads: int = 0,
-             per_root: bool = False, enumerate_: bool = False, cap: int | None = None):
-        """Run Algorithm 1.  Returns dict(count, stats, per_root?, rows?, n_total?)."""
+             per_root: bool = False, enumerate_: bool = False, cap: int | None = None,
+             vlabels=None, elabels=None, anti=None):
+        """Run Algorithm 1.  Returns dict(count, stats, per_root?, rows?, n_total?).
+        vlabels / elabels / anti: the generalized query's constraints
+        (make_constraints)."""
+        cons = make_constraints(vlabels, elabels, anti)
         lib = _load()
         L = len(motif)
         mu = np.array([e[0] for e in motif], np.uint32)
@@ -140,12 +191,13 @@ class Graph:
         if enumerate_:
             if cap is None:
                 cap = int(self.mine(motif, delta, fine, root_range=root_range, roots=roots,
-                                    threads=threads)["count"])
+                                    threads=threads, vlabels=vlabels, elabels=elabels, anti=anti)["count"])
             buf = np.zeros((max(cap, 1), L), np.uint32)
             ntot = np.zeros(1, np.uint64)
         cnt = np.zeros(1, np.uint64)
         st = Stats()
-        rc = lib.tmo_mine(self._h, L, _ptr(mu), _ptr(mv), int(delta), _ptr(fa), int(lo), int(hi),
+        rc = lib.tmo_mine(self._h, L, _ptr(mu), _ptr(mv), int(delta), _ptr(fa),
+                          None if cons is None else ctypes.byref(cons), int(lo), int(hi),
                           _ptr(ra), nr, int(threads), _ptr(cnt), _ptr(pr), _ptr(buf),
                           int(cap or 0), _ptr(ntot), ctypes.byref(st))
         if rc:

@@ -38,6 +38,18 @@
  *   Q9 a motif edge after the first that touches no earlier motif vertex
  *      (Alg. 1's "Both u_G, v_G not mapped" branch) is rejected.
  *
+ * Generalized query:
+ *   labels   vertex/edge labels are small integers (unlabeled = 0); a motif
+ *            vertex / motif edge may require an exact label (TMO_ANY = none).
+ *            Checked whenever a vertex or edge is newly matched.
+ *   anti     an anti-edge ¬(u_j, v_j, δ_ij) attached to real motif edge i
+ *            rejects a match if some graph edge φ(u_j) -> φ(v_j) has
+ *            t in [t(e_i), t(e_i) + δ_ij] (inclusive).  Reading Q22:
+ *            the witness must be an edge other than the match's own edges;
+ *            the check runs when the last real edge is matched (a witness
+ *            may lie after it), so it prunes nothing earlier.
+ *
+ *
  * Instrumentation (used to derive algorithmic bytes, and as a parity target
  * for the GPU's "every window is searched exactly once" invariant):
  *   nodes[l]    number of partial matches with l edges whose candidate list
@@ -55,6 +67,8 @@
 #define TMO_MAXL 8      /* motif edges */
 #define TMO_MAXV 16     /* motif vertex ids accepted: 0..15 */
 #define TMO_INF INT64_MAX
+#define TMO_MAXANTI 4
+#define TMO_ANY (-1)    /* no label requirement */
 
 enum { TMO_OK = 0, TMO_EINVAL = 1, TMO_ENOMEM = 2, TMO_EUNSUPPORTED = 3 };
 
@@ -66,7 +80,19 @@ typedef struct {
     uint64_t *perm;           /* perm[id] = position in caller's input      */
     uint64_t *out_off, *in_off;   /* "Two CSR-like data structures ... storing */
     uint64_t *out_e, *in_e;       /*  their indices in the temporal edge list" */
+    int32_t *vlab;            /* vertex labels (n) or NULL = all 0          */
+    int32_t *elab;            /* edge labels by sorted id (m) or NULL = all 0 */
 } tmo_graph;
+
+/* Constraints of the generalized query. */
+typedef struct {
+    int32_t vlabel[TMO_MAXV];            /* required label per motif vertex, TMO_ANY = none */
+    int32_t elabel[TMO_MAXL];            /* required label per motif edge                   */
+    uint32_t n_anti;
+    uint32_t anti_u[TMO_MAXANTI], anti_v[TMO_MAXANTI];   /* motif vertices                */
+    uint32_t anti_attach[TMO_MAXANTI];                    /* real motif edge, 0-based      */
+    int64_t anti_window[TMO_MAXANTI];                     /* δ_ij >= 0                     */
+} tmo_constraints;
 
 typedef struct {
     uint64_t nodes[TMO_MAXL];
@@ -91,6 +117,7 @@ void tmo_graph_free(tmo_graph *g) {
     if (!g) return;
     free(g->src); free(g->dst); free(g->t); free(g->perm);
     free(g->out_off); free(g->in_off); free(g->out_e); free(g->in_e);
+    free(g->vlab); free(g->elab);
     free(g);
 }
 
@@ -133,6 +160,28 @@ int tmo_graph_build(const uint32_t *src, const uint32_t *dst, const int64_t *t,
 
 uint64_t tmo_graph_m(const tmo_graph *g) { return g->m; }
 
+/* Optional labels ("nodes and edges can be optionally endowed with discrete
+ * attributes/labels"): vlab[n] per vertex, elab[m] per edge in the
+ * caller's INPUT order (stored by sorted id); NULL leaves that kind at 0. */
+int tmo_graph_set_labels(tmo_graph *g, const int32_t *vlab, const int32_t *elab) {
+    if (vlab) {
+        free(g->vlab);
+        g->vlab = malloc(((size_t)g->n + 1) * 4);
+        if (!g->vlab) return TMO_ENOMEM;
+        memcpy(g->vlab, vlab, (size_t)g->n * 4);
+    }
+    if (elab) {
+        free(g->elab);
+        g->elab = malloc((g->m ? g->m : 1) * 4);
+        if (!g->elab) return TMO_ENOMEM;
+        for (uint64_t e = 0; e < g->m; e++) g->elab[e] = elab[g->perm[e]];
+    }
+    return TMO_OK;
+}
+
+static int32_t vertex_label(const tmo_graph *g, uint32_t v) { return g->vlab ? g->vlab[v] : 0; }
+static int32_t edge_label(const tmo_graph *g, uint64_t e) { return g->elab ? g->elab[e] : 0; }
+
 /* sorted edge id -> input position, and the sorted arrays themselves */
 void tmo_graph_export(const tmo_graph *g, uint64_t *perm, uint32_t *src, uint32_t *dst, int64_t *t) {
     for (uint64_t e = 0; e < g->m; e++) {
@@ -156,6 +205,7 @@ typedef struct {
     uint32_t *enum_buf;          /* rows of L edge ids, may be NULL            */
     uint64_t cap;
     uint64_t *n_enum;            /* rows produced (written when < cap)         */
+    const tmo_constraints *cons; /* labels / anti-edges, NULL = none           */
 } tmo_query;
 
 typedef struct {
@@ -181,6 +231,54 @@ static int StructConstraints(const tmo_ctx *c, uint64_t e, int64_t uG, int64_t v
     int v_consistent = (vG == (int64_t)v2) || (vG < 0 && c->MapGM[v2] < 0);
     if (uG < 0 && vG < 0 && u2 == v2) return 0;
     return u_consistent && v_consistent;
+}
+
+/* Label checks of a candidate e for motif edge eM ("whenever a
+ * new vertex/edge is matched ... check their validity"): the edge's label,
+ * and the label of each endpoint this edge maps for the first time. */
+static int LabelConstraints(const tmo_ctx *c, uint64_t e, uint32_t eM, int64_t uG, int64_t vG) {
+    const tmo_constraints *k = c->q->cons;
+    if (!k) return 1;
+    if (k->elabel[eM] != TMO_ANY && edge_label(c->g, e) != k->elabel[eM]) return 0;
+    int32_t ru = k->vlabel[c->q->mu[eM]], rv = k->vlabel[c->q->mv[eM]];
+    if (uG < 0 && ru != TMO_ANY && vertex_label(c->g, c->g->src[e]) != ru) return 0;
+    if (vG < 0 && rv != TMO_ANY && vertex_label(c->g, c->g->dst[e]) != rv) return 0;
+    return 1;
+}
+
+/* Temporal anti-edges of the complete match eStack[0..L-2]
+ * + last: rejected if a graph edge φ(u_j) -> φ(v_j) other than the match's own
+ * edges (reading Q22) has t in [t(e_attach), t(e_attach) + δ_ij].  The
+ * out-list of φ(u_j) is sorted by (t, id): binary-search t >= t(e_attach),
+ * then scan while t <= t(e_attach) + δ_ij. */
+static int AntiConstraints(const tmo_ctx *c, uint64_t last) {
+    const tmo_constraints *k = c->q->cons;
+    if (!k || !k->n_anti) return 1;
+    const tmo_graph *g = c->g;
+    const tmo_query *q = c->q;
+    uint64_t match[TMO_MAXL];
+    int64_t phi[TMO_MAXV];
+    for (uint32_t i = 0; i + 1 < q->L; i++) match[i] = c->eStack[i];
+    match[q->L - 1] = last;
+    for (uint32_t i = 0; i < q->L; i++) { phi[q->mu[i]] = g->src[match[i]]; phi[q->mv[i]] = g->dst[match[i]]; }
+    for (uint32_t j = 0; j < k->n_anti; j++) {
+        uint32_t x = (uint32_t)phi[k->anti_u[j]], y = (uint32_t)phi[k->anti_v[j]];
+        int64_t ta = g->t[match[k->anti_attach[j]]], w = k->anti_window[j];
+        const uint64_t *list = g->out_e + g->out_off[x];
+        uint64_t len = g->out_off[x + 1] - g->out_off[x], lo = 0, hi = len;
+        while (lo < hi) {
+            uint64_t mid = lo + (hi - lo) / 2;
+            if (g->t[list[mid]] >= ta) hi = mid; else lo = mid + 1;
+        }
+        for (uint64_t p = lo; p < len && g->t[list[p]] - ta <= w; p++) {
+            uint64_t e = list[p];
+            if (g->dst[e] != y) continue;
+            int own = 0;
+            for (uint32_t i = 0; i < q->L; i++) own |= (match[i] == e);
+            if (!own) return 0;   /* the absence the anti-edge asks for is violated */
+        }
+    }
+    return 1;
 }
 
 /* UpdateDataStructures */
@@ -223,6 +321,7 @@ static uint32_t ceil_log2_plus1(uint64_t len) { /* ceil(log2(len+1)) */
 /* Output a motif H using eStack */
 static void emit(tmo_ctx *c, uint64_t last) {
     const tmo_query *q = c->q;
+    if (!AntiConstraints(c, last)) return;
     c->count++;
     if (q->count_slot) (*q->count_slot)++;
     if (q->enum_buf) {
@@ -269,6 +368,7 @@ static void search_level(tmo_ctx *c) {
         if (g->t[e] - tprev > fine) break;        /* fine-grained bound */
         c->st.window_sum++;
         if (!StructConstraints(c, e, uG, vG)) continue;
+        if (!LabelConstraints(c, e, eM, uG, vG)) continue;
         /* NextLevel */
         if (eM == q->L - 1) { emit(c, e); continue; }
         UpdateDataStructures(c, e, eM);
@@ -284,6 +384,7 @@ static void search_level(tmo_ctx *c) {
  * every graph edge). */
 static void mine_root(tmo_ctx *c, uint64_t r) {
     if (!StructConstraints(c, r, -1, -1)) return;   /* both endpoints unmapped */
+    if (!LabelConstraints(c, r, 0, -1, -1)) return;
     if (c->q->L == 1) { c->depth = 0; emit(c, r); return; }
     UpdateDataStructures(c, r, 0);
     c->eStack[0] = r; c->depth = 1;                 /* t' <- time(r) + δ */
@@ -313,16 +414,33 @@ static int validate(uint32_t L, const uint32_t *mu, const uint32_t *mv, int64_t 
  * rows of L sorted-edge ids in root order, lexicographic by construction;
  * *n_total gets the exact number of matches.  stats (nullable).
  * nthreads <= 0: OpenMP default. */
+/* Anti-edges: at most TMO_MAXANTI, endpoints distinct motif vertices of the
+ * motif, attached to a real edge, window >= 0. */
+static int validate_constraints(uint32_t L, const uint32_t *mu, const uint32_t *mv, const tmo_constraints *k) {
+    if (!k) return TMO_OK;
+    if (k->n_anti > TMO_MAXANTI) return TMO_EINVAL;
+    int seen[TMO_MAXV] = {0};
+    for (uint32_t i = 0; i < L; i++) seen[mu[i]] = seen[mv[i]] = 1;
+    for (uint32_t j = 0; j < k->n_anti; j++) {
+        if (k->anti_u[j] >= TMO_MAXV || k->anti_v[j] >= TMO_MAXV || k->anti_u[j] == k->anti_v[j]) return TMO_EINVAL;
+        if (!seen[k->anti_u[j]] || !seen[k->anti_v[j]]) return TMO_EINVAL;
+        if (k->anti_attach[j] >= L || k->anti_window[j] < 0) return TMO_EINVAL;
+    }
+    return TMO_OK;
+}
+
 int tmo_mine(const tmo_graph *g, uint32_t L, const uint32_t *mu, const uint32_t *mv,
-             int64_t delta, const int64_t *fine,
+             int64_t delta, const int64_t *fine, const tmo_constraints *cons,
              uint64_t root_lo, uint64_t root_hi, const uint64_t *roots, uint64_t n_roots,
              int nthreads, uint64_t *count, uint64_t *per_root,
              uint32_t *enum_buf, uint64_t cap, uint64_t *n_total, tmo_stats *stats) {
     int rc = validate(L, mu, mv, delta, fine);
     if (rc) return rc;
+    rc = validate_constraints(L, mu, mv, cons);
+    if (rc) return rc;
     tmo_query q;
     memset(&q, 0, sizeof q);
-    q.L = L; q.delta = delta;
+    q.L = L; q.delta = delta; q.cons = cons;
     for (uint32_t i = 0; i < L; i++) { q.mu[i] = mu[i]; q.mv[i] = mv[i]; }
     for (uint32_t i = 0; i < TMO_MAXL; i++) q.fine[i] = TMO_INF;
     if (fine) for (uint32_t i = 0; i + 1 < L; i++) q.fine[i] = fine[i];

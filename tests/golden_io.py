@@ -34,8 +34,17 @@ def load(path):
         fine = [INF if x == "inf" else int(x) for x in d["fine"].split()]
     rows = sorted(tuple(int(x) for x in g) for g in _groups(d["rows"]))
     n = max(src + dst) + 1 if src else 1
+    # generalized query (optional keys): anti: u v attach window | ...;
+    # vlab: label per graph vertex; elab: label per input edge;
+    # mvlabels: motif-vertex:label ...; melabels: per motif edge label or *
+    anti = [tuple(int(x) for x in g) for g in _groups(d["anti"])] if "anti" in d else None
+    vlab = [int(x) for x in d["vlab"].split()] if "vlab" in d else None
+    elab = [int(x) for x in d["elab"].split()] if "elab" in d else None
+    mvl = {int(a): int(b) for a, b in (x.split(":") for x in d["mvlabels"].split())} if "mvlabels" in d else None
+    mel = [None if x == "*" else int(x) for x in d["melabels"].split()] if "melabels" in d else None
     return dict(name=os.path.basename(path), src=src, dst=dst, t=t, n=n, motif=motif, delta=delta,
-                fine=fine, count=int(d["count"]), rows=rows)
+                fine=fine, count=int(d["count"]), rows=rows, anti=anti, vlab=vlab, elab=elab, vlabels=mvl,
+                elabels=mel)
 
 
 def all_fixtures():

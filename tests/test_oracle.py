@@ -28,13 +28,22 @@ def orows(src, dst, t, n, motif, delta, fine=None):
 
 
 # --------------------------------------------------------------- worked examples
+def fx_cons(fx):
+    return dict(vlabels=fx["vlabels"], elabels=fx["elabels"], anti=fx["anti"])
+
+
 @pytest.mark.parametrize("fx", all_fixtures(), ids=lambda f: f["name"])
 def test_golden(fx):
-    rows, n_total = orows(fx["src"], fx["dst"], fx["t"], fx["n"], fx["motif"], fx["delta"], fx["fine"])
-    assert n_total == fx["count"]
+    og = oracle.Graph(fx["src"], fx["dst"], fx["t"], fx["n"])
+    if fx["vlab"] is not None or fx["elab"] is not None:
+        og.set_labels(fx["vlab"], fx["elab"])
+    r = og.mine(fx["motif"], fx["delta"], fx["fine"], enumerate_=True, **fx_cons(fx))
+    rows = sorted(tuple(int(x) for x in row) for row in r["rows"])
+    assert r["n_total"] == fx["count"]
     assert rows == fx["rows"]
     # the fixture itself is consistent with the literal definition
-    assert brute(fx["src"], fx["dst"], fx["t"], fx["motif"], fx["delta"], fx["fine"]) == fx["rows"]
+    assert brute(fx["src"], fx["dst"], fx["t"], fx["motif"], fx["delta"], fx["fine"], vlab=fx["vlab"],
+                 elab=fx["elab"], **fx_cons(fx)) == fx["rows"]
 
 
 # ------------------------------------------------------------------ brute force
@@ -302,3 +311,84 @@ def test_c5_slices_agree_and_tile():
     assert np.all(r0[2][:n0] < tb) and np.all(r1[2] >= tb)
     assert len(halo) == np.searchsorted(r1[2], tb + 3600, "right")   # exactly the next δ-window
     assert np.array_equal(r0[0][n0:], r1[0][:len(halo)])
+
+
+
+# ------------------------------------------- generalized query: labels, anti-edges
+def random_constraints(rng, motif, n_labels):
+    """Random label requirements and anti-edges over the motif's vertices."""
+    verts = sorted({x for e in motif for x in e})
+    vl = {v: rng.randrange(n_labels) for v in verts if rng.random() < 0.3} or None
+    el = [rng.randrange(n_labels) if rng.random() < 0.25 else None for _ in motif]
+    el = el if any(x is not None for x in el) else None
+    anti = []
+    for _ in range(rng.choice([0, 0, 1, 1, 2])):
+        u, v = rng.sample(verts, 2)
+        anti.append((u, v, rng.randrange(len(motif)), rng.choice([0, 2, 5, 12, 40])))
+    return vl, el, anti or None
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_labels_and_anti_edges_vs_brute(seed):
+    """Oracle = the literal definition (brute force scanning the whole edge list
+    for anti-edge witnesses) on random small multigraphs with duplicate
+    timestamps, labels and up to two anti-edges per motif."""
+    rng = random.Random(4200 + seed)
+    for k in range(40):
+        n = rng.randint(2, 7)
+        src, dst, t, _ = synth.tiny_graph(seed * 1000 + k, n=n, m=rng.randint(0, 45), tmax=rng.randint(4, 40))
+        L = rng.choice([1, 2, 3, 3, 4])
+        motif = rng.choice([c for c in CATALOG if len(c) == L] + [random_motif(rng, L)])
+        nl = rng.choice([1, 2, 3])
+        vlab = [rng.randrange(nl) for _ in range(n)] if rng.random() < 0.7 else None
+        elab = [rng.randrange(nl) for _ in range(len(src))] if rng.random() < 0.5 else None
+        vl, el, anti = random_constraints(rng, motif, nl)
+        delta = rng.choice([0, 3, 10, 25, INF])
+        fine = random_fine(rng, L)
+        og = oracle.Graph(src, dst, t, n)
+        if vlab is not None or elab is not None:
+            og.set_labels(vlab, elab)
+        r = og.mine(motif, delta, fine, enumerate_=True, vlabels=vl, elabels=el, anti=anti)
+        got = sorted(tuple(int(x) for x in row) for row in r["rows"])
+        exp = brute(src, dst, t, motif, delta, fine, vlab=vlab, elab=elab, vlabels=vl, elabels=el, anti=anti)
+        assert got == exp, (seed, k, motif, delta, fine, vl, el, anti)
+
+
+def test_constraint_invariants():
+    """Invariants the definition implies: requirements can only remove matches;
+    an always-satisfied label requirement changes nothing; an anti-edge with a
+    pair the graph never has changes nothing; widening an anti window never
+    adds matches; all-distinct labels split the count exactly."""
+    src, dst, t, n = synth.tiny_graph(77, n=6, m=120, tmax=80)
+    og = oracle.Graph(src, dst, t, n)
+    base = og.mine(M.TRI, 30)["count"]
+    assert base > 0
+    og.set_labels([0] * n, [0] * len(src))
+    assert og.mine(M.TRI, 30, vlabels={0: 0, 1: 0, 2: 0}, elabels=[0, 0, 0])["count"] == base
+    # labels 0/1 per vertex: the counts over the 2^3 label assignments of the motif vertices sum to base
+    lab = [v % 2 for v in range(n)]
+    og.set_labels(lab, None)
+    tot = sum(og.mine(M.TRI, 30, vlabels={0: a, 1: b, 2: c})["count"] for a in (0, 1) for b in (0, 1) for c in (0, 1))
+    assert tot == base
+    # edge labels by input position parity, per motif edge: sums over assignments again
+    og.set_labels(None, [i % 2 for i in range(len(src))])
+    tot = sum(og.mine(M.TRI, 30, elabels=[a, b, c])["count"] for a in (0, 1) for b in (0, 1) for c in (0, 1))
+    assert tot == base
+    # anti-edges: monotone in the window, bounded by the unconstrained count
+    prev = base
+    for w in (0, 1, 3, 10, 30, 100):
+        c = og.mine(M.TRI, 30, anti=[(0, 2, 0, w)])["count"]
+        assert c <= prev
+        prev = c
+    # a vertex the graph never touches as a target: the anti pair never exists
+    src2 = np.concatenate([src, [n]]).astype(np.uint32)
+    dst2 = np.concatenate([dst, [0]]).astype(np.uint32)
+    t2 = np.concatenate([t, [10**6]]).astype(np.int64)
+    og2 = oracle.Graph(src2, dst2, t2, n + 1)
+    assert og2.mine(M.TRI, 30)["count"] == base
+    with pytest.raises(oracle.OracleError):
+        og.mine(M.TRI, 30, anti=[(0, 0, 0, 5)])
+    with pytest.raises(oracle.OracleError):
+        og.mine(M.TRI, 30, anti=[(0, 7, 0, 5)])
+    with pytest.raises(oracle.OracleError):
+        og.mine(M.TRI, 30, anti=[(0, 1, 3, 5)])
