@@ -112,6 +112,39 @@ tm_status tm_motif_create(uint32_t L, const uint32_t *mu, const uint32_t *mv, in
 
 tm_status tm_motif_destroy(tm_motif *mo);
 
+/* --------------------------------------------- generalized query (N2) */
+/* "Nodes and edges can be optionally endowed with discrete attributes/labels"
+ * (P:167); a generalized motif may require labels and carry temporal
+ * anti-edges.  Labels are int32 >= 0; unlabeled
+ * vertices/edges have label 0. */
+#define TM_ANY_LABEL (-1)   /* no requirement */
+#define TM_MAX_ANTI 4       /* anti-edges per motif */
+
+/* Attach labels to a graph: vlabels[n] per vertex, elabels[m] per edge in
+ * the caller's INPUT order (NULL: leave that kind at 0).  Pointers are host,
+ * or device when on_device.  The library copies them (edge labels into edge-id
+ * order).  Not concurrent with queries on g.  Errors: TM_EINVAL, TM_ENOMEM,
+ * TM_ECUDA. */
+tm_status tm_graph_set_labels(tm_graph *g, const int32_t *vlabels, const int32_t *elabels, int on_device);
+
+/* Require motif vertex `vertex` (the caller's label in mu/mv) to map to a
+ * graph vertex with `label`, or motif edge `edge` (0-based, list order) to
+ * match a graph edge with `label` (checked whenever the vertex /
+ * edge is newly matched).  label = TM_ANY_LABEL clears the requirement.
+ * Errors: TM_EINVAL (vertex not in the motif, edge >= L, label < -1). */
+tm_status tm_motif_set_vertex_label(tm_motif *mo, uint32_t vertex, int32_t label);
+tm_status tm_motif_set_edge_label(tm_motif *mo, uint32_t edge, int32_t label);
+
+/* Attach a temporal anti-edge ¬(u, v, window) to real motif edge `attach`
+ * (0-based): a match is rejected if the graph holds an edge
+ * φ(u) -> φ(v), other than the match's own edges (reading Q22), with
+ * t in [t(e_attach), t(e_attach) + window] (inclusive).  u, v: the caller's
+ * motif vertex labels, distinct, both in the motif.  Matches are checked when
+ * complete.  Motifs with labels or anti-edges run on the generic kernel.
+ * Errors: TM_EINVAL (bad vertex, attach >= L, window < 0, more than
+ * TM_MAX_ANTI anti-edges). */
+tm_status tm_motif_add_anti_edge(tm_motif *mo, uint32_t u, uint32_t v, uint32_t attach, int64_t window);
+
 /* Whether the motif runs on a compile-time specialised kernel (1) or on the
  * generic kernel with a runtime plan (0). */
 tm_status tm_motif_specialised(const tm_motif *mo, int *specialised);

@@ -19,6 +19,8 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
 void graph_destroy(tm_graph *g);
 cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, uint64_t *scratch, cudaStream_t s);
 cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s);
+cudaError_t build_tie_lo(const DeviceGraph &d, uint32_t *S, cudaStream_t s);
+tm_status set_labels(DeviceGraph &d, const int32_t *vl, const int32_t *el, bool on_device);
 size_t horizon_scratch_words(uint64_t m);
 
 namespace {
@@ -69,8 +71,8 @@ bool is_specialised(uint64_t code) {
     return false;
 }
 
-KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised) {
-    if (mode == kCount || mode == kEnum) {
+KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised, bool generic) {
+    if (!generic && (mode == kCount || mode == kEnum)) {
         for (auto &e : catalog())
             if (e.code == code) {
                 if (specialised) *specialised = true;
@@ -151,12 +153,17 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
     std::vector<std::array<int, kMaxL>> gap(k);
     std::vector<std::pair<int, int>> hkeys;   // window-end ranks: (list variant, horizon index)
     std::vector<std::array<int, kMaxL>> hwhich(k);
+    std::vector<std::array<int, TM_MAX_ANTI>> anti_h(k);   // horizon index of each anti-edge window
+    bool need_tie = false;                                 // tie_lo: first id of each timestamp
     for (uint32_t i = 0; i < k; i++) {
         const tm_motif *mo = mos[i];
         gap[i].fill(-1);
         hwhich[i].fill(-1);
-        if (mo->L < 2 || base.n_roots == 0) continue;
+        anti_h[i].fill(-1);
+        if ((mo->L < 2 && !mo->n_anti) || base.n_roots == 0) continue;
         dl[i] = hidx(mo->delta);
+        for (uint32_t j = 0; j < mo->n_anti; j++) anti_h[i][j] = hidx(mo->anti_window[j]);
+        if (mo->n_anti) need_tie = true;
         for (uint32_t j = 0; j + 1 < mo->L; j++) {
             const int64_t f = mo->fine[j];
             if (f == TM_DELTA_INF || f >= mo->delta) continue;
@@ -208,11 +215,20 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         TM_CUDA_TRY(dev_alloc((void **)&hrbuf, hkeys.size() * m * sizeof(uint32_t), s));
         fr.v.push_back(hrbuf);
     }
+    uint32_t *tie = nullptr;
+    if (need_tie && m) {
+        TM_CUDA_TRY(dev_alloc((void **)&tie, m * sizeof(uint32_t), s));
+        fr.v.push_back(tie);
+    }
 
     TM_CUDA_TRY(cudaEventRecord(ev0, s));
     for (size_t i = 0; i < hv.size(); i++) {
         TM_CUDA_TRY(build_horizon(d, hv[i], hbuf + i * m, hscr, s));
         g_info.launches += 2;
+    }
+    if (tie) {
+        TM_CUDA_TRY(build_tie_lo(d, tie, s));
+        g_info.launches++;
     }
     if (!hkeys.empty()) {
         if (TM_HRANK == 2) {   // memo: 0 = not yet known
@@ -238,6 +254,21 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         p.L = mo->L;
         for (uint32_t j = 0; j < mo->L; j++) { p.u[j] = mo->u[j]; p.v[j] = mo->v[j]; }
         p.scratch = scratch + (size_t)i * kScratchWords;
+        if (mo->constrained()) {   // generalized query: the generic kernel checks labels and anti-edges
+            p.gen = 1;
+            p.vlab = d.vlab;
+            p.elab = d.elab;
+            for (int j = 0; j < kMaxV; j++) p.vreq[j] = mo->vreq[j];
+            for (int j = 0; j < kMaxL; j++) p.ereq[j] = mo->ereq[j];
+            p.n_anti = mo->n_anti;
+            for (uint32_t j = 0; j < mo->n_anti; j++) {
+                p.anti_u[j] = mo->anti_u[j];
+                p.anti_v[j] = mo->anti_v[j];
+                p.anti_a[j] = mo->anti_attach[j];
+                p.anti_hi[j] = dl[i] >= 0 ? hbuf + (size_t)anti_h[i][j] * m : nullptr;
+            }
+            p.tie_lo = tie;
+        }
         if (dl[i] >= 0) {
             p.H = hbuf + (size_t)dl[i] * m;
             for (uint32_t j = 0; j + 1 < mo->L; j++) {
@@ -247,7 +278,7 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         }
         if (p.n_roots > 0) {
             bool spec = false;
-            KernelInfo ki = lookup_kernel(mo->code, mode, &spec);
+            KernelInfo ki = lookup_kernel(mo->code, mode, &spec, mo->constrained());
             const size_t smem = (size_t)ki.smem_per_warp * kWarpsPerBlock;
             {
                 std::lock_guard<std::mutex> lk(g_attr_mu);
@@ -453,6 +484,9 @@ tm_status tm_motif_create(uint32_t L, const uint32_t *mu, const uint32_t *mv, in
         mo.v[i] = (uint8_t)label[mv[i]];
     }
     mo.nv = nv;
+    for (int i = 0; i < 64; i++) mo.internal[i] = (int8_t)label[i];
+    for (int i = 0; i < kMaxV; i++) mo.vreq[i] = TM_ANY_LABEL;
+    for (int i = 0; i < kMaxL; i++) mo.ereq[i] = TM_ANY_LABEL;
     for (int i = 0; i < kMaxL; i++) mo.fine[i] = TM_DELTA_INF;
     if (fine)
         for (uint32_t i = 0; i + 1 < L; i++) {
@@ -469,6 +503,45 @@ tm_status tm_motif_create(uint32_t L, const uint32_t *mu, const uint32_t *mv, in
 tm_status tm_motif_destroy(tm_motif *mo) {
     delete mo;
     return TM_OK;
+}
+
+tm_status tm_motif_set_vertex_label(tm_motif *mo, uint32_t vertex, int32_t label) {
+    g_err.clear();
+    if (!mo || vertex >= 64 || mo->internal[vertex] < 0) return fail(TM_EINVAL, "vertex is not in the motif");
+    if (label < TM_ANY_LABEL) return fail(TM_EINVAL, "label < -1");
+    mo->vreq[mo->internal[vertex]] = label;
+    return TM_OK;
+}
+
+tm_status tm_motif_set_edge_label(tm_motif *mo, uint32_t edge, int32_t label) {
+    g_err.clear();
+    if (!mo || edge >= mo->L) return fail(TM_EINVAL, "edge >= L");
+    if (label < TM_ANY_LABEL) return fail(TM_EINVAL, "label < -1");
+    mo->ereq[edge] = label;
+    return TM_OK;
+}
+
+tm_status tm_motif_add_anti_edge(tm_motif *mo, uint32_t u, uint32_t v, uint32_t attach, int64_t window) {
+    g_err.clear();
+    if (!mo) return fail(TM_EINVAL, "null motif");
+    if (mo->n_anti >= TM_MAX_ANTI) return fail(TM_EINVAL, "more than TM_MAX_ANTI anti-edges");
+    if (u >= 64 || v >= 64 || mo->internal[u] < 0 || mo->internal[v] < 0 || u == v)
+        return fail(TM_EINVAL, "anti-edge endpoints must be distinct motif vertices");
+    if (attach >= mo->L) return fail(TM_EINVAL, "attach >= L");
+    if (window < 0 || window == TM_DELTA_INF) return fail(TM_EINVAL, "anti-edge window must be finite and >= 0");
+    const uint32_t j = mo->n_anti++;
+    mo->anti_u[j] = (uint8_t)mo->internal[u];
+    mo->anti_v[j] = (uint8_t)mo->internal[v];
+    mo->anti_attach[j] = (uint8_t)attach;
+    mo->anti_window[j] = window;
+    return TM_OK;
+}
+
+tm_status tm_graph_set_labels(tm_graph *g, const int32_t *vlabels, const int32_t *elabels, int on_device) {
+    g_err.clear();
+    if (!g) return fail(TM_EINVAL, "null graph");
+    DeviceGuard guard(g->device);
+    return set_labels(g->d, vlabels, elabels, on_device != 0);
 }
 
 tm_status tm_motif_specialised(const tm_motif *mo, int *sp) {

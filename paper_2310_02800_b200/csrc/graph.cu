@@ -233,7 +233,8 @@ cudaError_t dmalloc(T **p, size_t count, cudaStream_t s) {
 
 void free_graph(DeviceGraph &d, cudaStream_t s) {
     for (void *q : {(void *)d.src, (void *)d.dst, (void *)d.t, (void *)d.perm, (void *)d.off_out, (void *)d.off_in,
-                    (void *)d.rec, (void *)d.rank, (void *)d.prec, (void *)d.ptab, (void *)d.pbits})
+                    (void *)d.rec, (void *)d.rank, (void *)d.prec, (void *)d.ptab, (void *)d.pbits,
+                    (void *)d.vlab, (void *)d.elab})
         dev_free(q, s);
     d = DeviceGraph{};
 }
@@ -420,6 +421,63 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
     }
 }
 }  // namespace
+
+namespace {
+// S[e] = the first edge id with the same timestamp as e: the anti-edge
+// window [t(e), t(e) + δ_ij] starts there in id order (reading Q1
+// orders equal timestamps by input position, so a witness may precede e).
+__global__ void k_tie_lo(const int64_t *__restrict__ T, uint64_t m, uint32_t *__restrict__ S) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const int64_t te = T[e];
+        if (e == 0 || T[e - 1] < te) { S[e] = (uint32_t)e; continue; }
+        uint64_t lo = 0, hi = e;   // first j in [0, e] with T[j] == te
+        while (lo < hi) {
+            const uint64_t mid = lo + ((hi - lo) >> 1);
+            if (T[mid] < te) lo = mid + 1;
+            else hi = mid;
+        }
+        S[e] = (uint32_t)lo;
+    }
+}
+
+__global__ void k_gather_i32(const int32_t *__restrict__ in, const uint32_t *__restrict__ perm, uint64_t m,
+                             int32_t *__restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) out[e] = in[perm[e]];
+}
+}  // namespace
+
+cudaError_t build_tie_lo(const DeviceGraph &d, uint32_t *S, cudaStream_t s) {
+    if (!d.m) return cudaSuccess;
+    k_tie_lo<<<grid_for(d.m), 256, 0, s>>>(d.t, d.m, S);
+    return cudaGetLastError();
+}
+
+// tm_graph_set_labels: vertex labels as given, edge labels permuted from the
+// caller's input order into edge-id order (perm[id] = input position).
+tm_status set_labels(DeviceGraph &d, const int32_t *vl, const int32_t *el, bool on_device) {
+    cudaStream_t s = nullptr;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (vl && d.n) {
+        if (!d.vlab) TM_CUDA_TRY(dmalloc(&d.vlab, (size_t)d.n, s));
+        TM_CUDA_TRY(cudaMemcpyAsync(d.vlab, vl, (size_t)d.n * 4, kind, s));
+    }
+    if (el && d.m) {
+        int32_t *tmp = nullptr;
+        TM_CUDA_TRY(dmalloc(&tmp, d.m, s));
+        cudaError_t e = cudaMemcpyAsync(tmp, el, d.m * 4, kind, s);
+        if (e == cudaSuccess && !d.elab) e = dmalloc(&d.elab, d.m, s);
+        if (e == cudaSuccess) {
+            k_gather_i32<<<grid_for(d.m), 256, 0, s>>>(tmp, d.perm, d.m, d.elab);
+            e = cudaGetLastError();
+        }
+        dev_free(tmp, s);
+        TM_CUDA_TRY(e);
+    }
+    TM_CUDA_TRY(cudaStreamSynchronize(s));
+    return TM_OK;
+}
 
 cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s) {
     if (!d.m) return cudaSuccess;

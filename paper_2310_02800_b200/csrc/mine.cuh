@@ -276,6 +276,7 @@ __host__ __device__ constexpr Shape shape_of() {
 // motif-specific code.
 template <uint64_t CODE>
 struct PlanC {
+    static constexpr bool kGeneral = false;   // labels / anti-edges: generic plan only
     static constexpr int kL = shape_of<CODE>().L;
     // φ slots stored with a level-l task
     __host__ __device__ static constexpr int nslots(int l) { return shape_of<CODE>().nv(l); }
@@ -300,6 +301,7 @@ struct PlanC {
 // L <= kMaxL edges, the decode computed per thread from the launch
 // parameters.
 struct PlanR {
+    static constexpr bool kGeneral = true;
     static constexpr int kL = kMaxL;
     __host__ __device__ static constexpr int nslots(int l) { return l + 1 < kMaxV ? l + 1 : kMaxV; }
     __host__ __device__ static constexpr bool keep_phi(int l, int k) { return k < nslots(l); }
@@ -435,6 +437,49 @@ struct Warp {
         return ok;
     }
 
+    // ------------------------------------------ generalized query (N2, PlanR)
+    __device__ __forceinline__ bool gen() const { return Plan::kGeneral && p.gen; }
+    __device__ __forceinline__ int32_t vlabel(uint32_t v) const { return p.vlab ? __ldg(p.vlab + v) : 0; }
+    __device__ __forceinline__ int32_t elabel(uint32_t e) const { return p.elab ? __ldg(p.elab + e) : 0; }
+
+    // Label checks of graph edge e matched to motif edge l, w its endpoint
+    // mapped for the first time (motif vertex nb), if any.
+    __device__ __forceinline__ bool labels_ok(int l, uint32_t e, bool fresh, int nb, uint32_t w) const {
+        if (p.ereq[l] != TM_ANY_LABEL && elabel(e) != p.ereq[l]) return false;
+        if (fresh && p.vreq[nb] != TM_ANY_LABEL && vlabel(w) != p.vreq[nb]) return false;
+        return true;
+    }
+
+    // Temporal anti-edges of a complete match: φ = phi
+    // (every motif vertex), matched edges eh[0..L-2] and e.  Rejected if the
+    // out-list of φ(u_j) holds an edge to φ(v_j), other than the match's own
+    // (reading Q22), with id in [tie_lo[e_a], H_{δ_ij}[e_a]] — i.e. with
+    // t in [t(e_a), t(e_a) + δ_ij].
+    template <int NS, int NE>
+    __device__ bool anti_ok(const uint32_t (&phi)[NS], const uint32_t (&eh)[NE], uint32_t e) const {
+        const int L = plan.L();
+        for (uint32_t j = 0; j < p.n_anti; j++) {
+            const uint32_t x = pick(phi, p.anti_u[j]), y = pick(phi, p.anti_v[j]);
+            const int a = p.anti_a[j];
+            const uint32_t ea = a == L - 1 ? e : pick(eh, a);
+            const uint32_t lo_id = __ldg(p.tie_lo + ea), hi_id = __ldg(p.anti_hi[j] + ea);
+            const uint32_t b = __ldg(p.off_out + x), en = __ldg(p.off_out + x + 1) - 1;
+            uint32_t q = lo_id ? first_after(p.rec, b, en, lo_id - 1) : b;
+            for (;; ++q) {   // the list's sentinel (id 0xFFFFFFFF) ends the scan
+                const uint64_t r = __ldg(p.rec + q);
+                const uint32_t id = (uint32_t)(r >> 32);
+                if (id > hi_id) break;
+                if ((uint32_t)r != y) continue;
+                bool own = id == e;
+#pragma unroll
+                for (int i = 0; i < NE; i++)
+                    if (i < L - 1 && eh[i] == id) own = true;
+                if (!own) return false;
+            }
+        }
+        return true;
+    }
+
     // enumerate one match found by a leaf scan: eh[0..nl-2], e, last
     template <int NE>
     __device__ __forceinline__ void emit_one(const uint32_t (&eh)[NE], uint32_t e, uint32_t last, int nl) {
@@ -558,7 +603,8 @@ struct Warp {
                 uint32_t pp = lo;
                 bool done = false;
                 uint32_t cnt = 0;
-                const bool leaf = NL + 1 == plan.L();
+                // (generalized queries check every match in expand(): no in-lane leaf scans)
+                const bool leaf = NL + 1 == plan.L() && !gen();
                 // leaf parent: the last motif edge's window is scanned in this
                 // lane and its matches counted (or emitted) on the spot, for up
                 // to kLeafSectors sectors; non-leaf: one sector to size the window
@@ -653,9 +699,16 @@ struct Warp {
             a = __ldg(p.src + r);
             bb = __ldg(p.dst + r);
             ok = a != bb;   // a self-loop cannot map two distinct motif vertices (Q4)
+            if (gen() && ok)
+                ok = labels_ok(0, r, true, 1, bb) && (p.vreq[0] == TM_ANY_LABEL || vlabel(a) == p.vreq[0]);
         }
         const uint32_t eh[1] = {r};
         if (plan.L() == 1) {
+            if (gen() && ok && p.n_anti) {
+                const uint32_t phi1[2] = {a, bb};
+                const uint32_t none[1] = {0};
+                ok = anti_ok(phi1, none, r);
+            }
             emit(ok, eh, r, (uint32_t)slot);
         } else if constexpr (LM > 1) {
             const uint32_t phi[2] = {a, bb};
@@ -721,6 +774,10 @@ struct Warp {
                 e = (uint32_t)(rc >> 32);
                 w = (uint32_t)rc;
                 ok = accept<LV>(w, pos < p.split, phi);
+                if (gen() && ok) {
+                    const int nb = plan.template nv<LV>();
+                    ok = labels_ok(LV, e, nb < plan.template nv<LV + 1>(), nb, w);
+                }
             }
         }
         __syncwarp();
@@ -731,6 +788,17 @@ struct Warp {
         __syncwarp();
 
         if (LV + 1 == plan.L()) {
+            if (gen() && ok && p.n_anti) {   // the complete match: φ with the last edge's new vertex
+                const int nb = plan.template nv<LV>();
+                uint32_t phiF[S + 2];
+#pragma unroll
+                for (int k = 0; k < S + 1; k++) phiF[k] = phi[k];
+                phiF[S + 1] = 0;
+#pragma unroll
+                for (int k = 0; k < S + 2; k++)
+                    if (k == nb && nb < plan.template nv<LV + 1>()) phiF[k] = w;
+                ok = anti_ok(phiF, eh, e);
+            }
             emit(ok, eh, e, rslot);
         } else if constexpr (LV + 1 < LM) {
             const int nb = plan.template nv<LV>();

@@ -54,6 +54,8 @@ struct DeviceGraph {
     // an absent pair — the common case when closing a cycle — costs one L2 hit
     uint32_t *pbits = nullptr;
     uint32_t fmask = 0;
+    // optional labels (tm_graph_set_labels): per vertex, per edge by sorted id
+    int32_t *vlab = nullptr, *elab = nullptr;
 };
 
 // Which motif edges with both endpoints mapped (closing edges) read
@@ -128,6 +130,19 @@ struct tm_motif {
     int64_t delta = 0;
     int64_t fine[tmg::kMaxL] = {};                    // gap i between edges i and i+1 (0-based)
     uint64_t code = 0;       // packed structure, selects the specialised kernel
+    int8_t internal[64];     // caller's motif vertex label -> internal vertex (-1: not in the motif)
+    // generalized query: label requirements and anti-edges
+    int32_t vreq[tmg::kMaxV];                         // per internal vertex, TM_ANY_LABEL = none
+    int32_t ereq[tmg::kMaxL];                         // per motif edge
+    uint32_t n_anti = 0;
+    uint8_t anti_u[TM_MAX_ANTI] = {}, anti_v[TM_MAX_ANTI] = {}, anti_attach[TM_MAX_ANTI] = {};
+    int64_t anti_window[TM_MAX_ANTI] = {};
+    bool constrained() const {
+        if (n_anti) return true;
+        for (uint32_t i = 0; i < nv; i++) if (vreq[i] != TM_ANY_LABEL) return true;
+        for (uint32_t i = 0; i < L; i++) if (ereq[i] != TM_ANY_LABEL) return true;
+        return false;
+    }
 };
 
 namespace tmg {
@@ -177,6 +192,14 @@ struct MineParams {
     uint32_t *qrec;
     uint32_t qmask;
     uint32_t total_warps;
+    // generalized query (PlanR only, gen != 0): labels and anti-edges
+    int gen;
+    const int32_t *vlab, *elab;        // graph labels (nullptr = all 0)
+    int32_t vreq[kMaxV], ereq[kMaxL];  // TM_ANY_LABEL = no requirement
+    uint32_t n_anti;
+    uint8_t anti_u[TM_MAX_ANTI], anti_v[TM_MAX_ANTI], anti_a[TM_MAX_ANTI];
+    const uint32_t *anti_hi[TM_MAX_ANTI];   // H_{δ_ij}: last id with t <= t(e) + δ_ij
+    const uint32_t *tie_lo;            // first id with t == t(e): the window [t(e), ...] starts there
     // runtime plan (generic kernel)
     uint32_t L;
     uint8_t u[kMaxL], v[kMaxL];
@@ -214,7 +237,7 @@ struct KernelInfo {
 };
 
 // catalog lookup: specialised kernel for `code` in `mode`, else the generic one
-KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised);
+KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised, bool generic = false);
 bool is_specialised(uint64_t code);
 
 // Device memory of the library: a per-device CUDA memory pool that keeps

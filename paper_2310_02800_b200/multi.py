@@ -14,11 +14,17 @@ import numpy as np
 from . import tmotif as T
 
 
-def reach(delta: int, fine=None) -> int:
-    """Largest possible t(e_L) - t(e_1) of a match: min(δ, Σ δ_i)."""
+def reach(delta: int, fine=None, anti=None) -> int:
+    """How far past its root a search tree reads: the largest t(e_L) - t(e_1)
+    of a match, min(δ, Σ δ_i), plus the longest anti-edge window (a witness
+    may lie up to δ_ij after its attached edge)."""
     if fine is None or any(f is None or f >= T.DELTA_INF for f in fine):
-        return int(delta)
-    return int(min(delta, sum(int(f) for f in fine)))
+        r = int(delta)
+    else:
+        r = int(min(delta, sum(int(f) for f in fine)))
+    if anti:
+        r += max(int(a[3]) for a in anti)
+    return r
 
 
 def rank_slice(t_sorted, reach_s: int, world: int, rank: int, weights=None):

@@ -72,6 +72,10 @@ SIGNATURES = [
     ("tm_graph_sorted_edges", _i32, [_P, _P, _P, _P]),
     ("tm_motif_create", _i32, [_u32, _P, _P, _i64, _P, ctypes.POINTER(_P)]),
     ("tm_motif_destroy", _i32, [_P]),
+    ("tm_graph_set_labels", _i32, [_P, _P, _P, _i32]),
+    ("tm_motif_set_vertex_label", _i32, [_P, _u32, _i32]),
+    ("tm_motif_set_edge_label", _i32, [_P, _u32, _i32]),
+    ("tm_motif_add_anti_edge", _i32, [_P, _u32, _u32, _u32, _i64]),
     ("tm_motif_specialised", _i32, [_P, ctypes.POINTER(_i32)]),
     ("tm_run_opts_default", None, [ctypes.POINTER(RunOpts)]),
     ("tm_count", _i32, [_P, _P, ctypes.POINTER(RunOpts), ctypes.POINTER(_u64)]),
@@ -193,6 +197,26 @@ class Graph:
 
     __del__ = close
 
+    def set_labels(self, vlabels=None, elabels=None):
+        """Vertex labels (n) and edge labels (m, the caller's input order);
+        numpy / host or torch CUDA int32 tensors; None leaves that kind at 0."""
+        on_dev = _is_torch(vlabels) or _is_torch(elabels)
+        conv = []
+        for x, k in ((vlabels, self.n), (elabels, self.m)):
+            if x is None:
+                conv.append(None)
+                continue
+            if on_dev:
+                import torch
+                x = x.to(torch.int32).contiguous()
+            else:
+                x = np.ascontiguousarray(x, np.int32)
+            if int(x.shape[0]) != k:
+                raise ValueError("label array length")
+            conv.append(x)
+        _check(lib().tm_graph_set_labels(self._h, None if conv[0] is None else _ptr(conv[0]),
+                                         None if conv[1] is None else _ptr(conv[1]), int(on_dev)))
+
     def sorted_to_input(self) -> np.ndarray:
         perm = np.empty(self.m, np.uint64)
         _check(lib().tm_graph_sorted_to_input(self._h, _host_ptr(perm)))
@@ -207,7 +231,9 @@ class Graph:
 class Motif:
     """tm_motif: ordered motif edges + δ + optional per-gap δ_i."""
 
-    def __init__(self, edges, delta: int, fine=None):
+    def __init__(self, edges, delta: int, fine=None, *, vlabels=None, elabels=None, anti=None):
+        """vlabels: {motif vertex: label}; elabels: per motif edge label or
+        None; anti: [(u, v, attach, window)] (generalized query)."""
         L = len(edges)
         mu = np.array([int(e[0]) for e in edges], np.uint32)
         mv = np.array([int(e[1]) for e in edges], np.uint32)
@@ -220,6 +246,13 @@ class Motif:
         _check(lib().tm_motif_create(L, _host_ptr(mu), _host_ptr(mv), int(delta),
                                      None if fa is None else _host_ptr(fa), ctypes.byref(h)))
         self._h = h
+        for v, lab in (vlabels or {}).items():
+            _check(lib().tm_motif_set_vertex_label(h, int(v), int(lab)))
+        for i, lab in enumerate(elabels or []):
+            if lab is not None:
+                _check(lib().tm_motif_set_edge_label(h, i, int(lab)))
+        for (u, v, a, w) in (anti or []):
+            _check(lib().tm_motif_add_anti_edge(h, int(u), int(v), int(a), int(w)))
         self.L = L
         self.edges = [tuple(e) for e in edges]
         self.delta = delta

@@ -64,7 +64,10 @@ def check_case(src, dst, t, n, motif, delta, fine, *, rows=True, stats=True, roo
 @pytest.mark.parametrize("fx", all_fixtures(), ids=lambda f: f["name"])
 def test_golden(fx):
     g = T.Graph(np.array(fx["src"]), np.array(fx["dst"]), np.array(fx["t"]), fx["n"])
-    mo = T.Motif(fx["motif"], fx["delta"], fx["fine"])
+    if fx["vlab"] is not None or fx["elab"] is not None:
+        g.set_labels(fx["vlab"], fx["elab"])
+    mo = T.Motif(fx["motif"], fx["delta"], fx["fine"], vlabels=fx["vlabels"], elabels=fx["elabels"],
+                 anti=fx["anti"])
     assert T.tm_count(g, mo) == fx["count"]
     r, n_total = gpu_rows(g, mo, cap=max(fx["count"], 1))
     assert n_total == fx["count"] and r == fx["rows"]
@@ -421,3 +424,105 @@ def test_count_multi_matches_single_queries_and_oracle():
         oo = oracle.Graph(s_, d_, t_, n_)
         res = T.tm_count_multi(gg, [T.Motif(mm, dd, ff) for mm, dd, ff in zip(ms, dls, fs)])
         assert res == [oo.mine(mm, dd, ff)["count"] for mm, dd, ff in zip(ms, dls, fs)]
+
+
+
+# ------------------------------- generalized query: labels and anti-edges (N2)
+def _cons_case(rng, motif, n_labels):
+    verts = sorted({x for e in motif for x in e})
+    vl = {v: rng.randrange(n_labels) for v in verts if rng.random() < 0.3} or None
+    el = [rng.randrange(n_labels) if rng.random() < 0.25 else None for _ in motif]
+    el = el if any(x is not None for x in el) else None
+    anti = [tuple(rng.sample(verts, 2)) + (rng.randrange(len(motif)), rng.choice([0, 2, 5, 12, 40]))
+            for _ in range(rng.choice([0, 1, 1, 2]))] or None
+    return vl, el, anti
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_labels_and_anti_edges_tiny_vs_oracle(seed):
+    """Counts, canonical enumeration, per-root counts and search-tree counters
+    of generalized queries (labels + anti-edges) against the oracle."""
+    rng = random.Random(5200 + seed)
+    for k in range(25):
+        n = rng.randint(2, 8)
+        src, dst, t, _ = synth.tiny_graph(seed * 1000 + k, n=n, m=rng.randint(0, 90), tmax=rng.randint(4, 40))
+        L = rng.choice([1, 2, 3, 3, 4, 5])
+        motif = rng.choice([c for c in CATALOG if len(c) == L] + [random_motif(rng, L)])
+        nl = rng.choice([1, 2, 3])
+        vlab = [rng.randrange(nl) for _ in range(n)] if rng.random() < 0.7 else None
+        elab = [rng.randrange(nl) for _ in range(len(src))] if rng.random() < 0.5 else None
+        vl, el, anti = _cons_case(rng, motif, nl)
+        delta = rng.choice([0, 3, 10, 25, INF])
+        fine = random_fine(rng, L)
+        og = oracle.Graph(src, dst, t, n)
+        g = T.Graph(src, dst, t, n)
+        if vlab is not None or elab is not None:
+            og.set_labels(vlab, elab)
+            g.set_labels(vlab, elab)
+        exp = og.mine(motif, delta, fine, enumerate_=True, vlabels=vl, elabels=el, anti=anti)
+        mo = T.Motif(motif, delta, fine, vlabels=vl, elabels=el, anti=anti)
+        ctx = (seed, k, motif, delta, fine, vl, el, anti)
+        assert T.tm_count(g, mo) == exp["count"], ctx
+        rows, n_total = gpu_rows(g, mo)
+        assert n_total == exp["n_total"], ctx
+        assert rows == [tuple(int(x) for x in r) for r in exp["rows"]], ctx
+        if len(src):
+            allr = np.arange(len(src), dtype=np.uint64)
+            pr = og.mine(motif, delta, fine, roots=allr, per_root=True, vlabels=vl, elabels=el, anti=anti)
+            assert np.array_equal(T.tm_count_roots(g, mo, allr), pr["per_root"]), ctx
+        st = T.tm_search_stats_run(g, mo)
+        assert st["nodes"][:L] == exp["stats"]["nodes"][:L], ctx
+        assert st["window_sum"] == exp["stats"]["window_sum"], ctx
+
+
+def test_labels_and_anti_edges_at_scale():
+    """A 400k-edge wiki-talk-shaped graph with 3 random vertex labels and 2
+    edge labels: the Table 5 style V / V+T / V+T+A queries on the 4-cycle and
+    the triangle against the oracle, through tm_count and tm_count_multi
+    (which shares the anti-edge horizons with the motifs' own)."""
+    src, dst, t, n = synth.config_graph("C3", m=400_000)
+    rng = np.random.default_rng(5)
+    vlab = rng.integers(0, 3, n).astype(np.int32)
+    elab = rng.integers(0, 2, len(src)).astype(np.int32)
+    og = oracle.Graph(src, dst, t, n)
+    og.set_labels(vlab, elab)
+    g = T.Graph(src, dst, t, n)
+    g.set_labels(vlab, elab)
+    day = 86400
+    cases = [(M.C4, day, None, {0: 0, 2: 1}, None, None),                          # V
+             (M.C4, day, [6 * 3600] * 3, {0: 0, 2: 1}, None, None),                # V+T
+             (M.C4, day, [6 * 3600] * 3, {0: 0, 2: 1}, None, [(2, 0, 2, 3600)]),   # V+T+A (P:632: anti 2->0 on edge 2)
+             (M.TRI, day, None, None, [1, None, 0], [(1, 0, 0, 7200), (0, 2, 2, 600)]),
+             (M.P3, 3600, None, None, None, [(3, 0, 2, 1800)])]
+    mos, exps = [], []
+    for mot, d, f, vl, el, anti in cases:
+        exp = og.mine(mot, d, f, vlabels=vl, elabels=el, anti=anti)["count"]
+        mo = T.Motif(mot, d, f, vlabels=vl, elabels=el, anti=anti)
+        assert T.tm_count(g, mo) == exp, (mot, d, f, vl, el, anti)
+        mos.append(mo)
+        exps.append(exp)
+    assert T.tm_count_multi(g, mos) == exps
+    # a device-side labelled copy (torch tensors) agrees
+    import torch
+    gd = T.Graph(torch.from_numpy(src.astype(np.int32)).cuda(), torch.from_numpy(dst.astype(np.int32)).cuda(),
+                 torch.from_numpy(t).cuda(), n)
+    gd.set_labels(torch.from_numpy(vlab).cuda(), torch.from_numpy(elab).cuda())
+    assert T.tm_count(gd, mos[2]) == exps[2]
+
+
+def test_generalized_query_errors():
+    g = T.Graph(np.array([0, 1], np.uint32), np.array([1, 2], np.uint32), np.array([0, 1], np.int64), 3)
+    with pytest.raises(T.TMotifError):
+        T.Motif(M.P3, 10, anti=[(0, 0, 0, 5)])
+    with pytest.raises(T.TMotifError):
+        T.Motif(M.P3, 10, anti=[(0, 9, 0, 5)])
+    with pytest.raises(T.TMotifError):
+        T.Motif(M.P3, 10, anti=[(0, 1, 3, 5)])
+    with pytest.raises(T.TMotifError):
+        T.Motif(M.P3, 10, anti=[(0, 1, 0, -1)])
+    with pytest.raises(T.TMotifError):
+        T.Motif(M.P3, 10, vlabels={7: 1})
+    with pytest.raises(T.TMotifError):
+        T.Motif(M.P3, 10, elabels=[0, 0, 0, 0])
+    with pytest.raises(ValueError):
+        g.set_labels([0, 1])
