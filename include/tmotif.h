@@ -145,6 +145,17 @@ tm_status tm_motif_set_edge_label(tm_motif *mo, uint32_t edge, int32_t label);
  * TM_MAX_ANTI anti-edges). */
 tm_status tm_motif_add_anti_edge(tm_motif *mo, uint32_t u, uint32_t v, uint32_t attach, int64_t window);
 
+/* Runtime specialisation ("code generator ... compiled into a
+ * shared library"): compiles, with NVRTC, the mining
+ * kernel template instantiated for this motif's structure (and, if the motif
+ * has labels or anti-edges, with those checks) for counting and enumeration,
+ * and uses it for every later query of mo.  A motif in the build-time catalog
+ * without constraints is already specialised (no-op).  Blocking, ~1-2 s per
+ * kernel on first use, cached per process.  Changing labels / anti-edges
+ * afterwards drops the specialisation.  Errors: TM_EINVAL, TM_ECUDA (with the
+ * NVRTC log in tm_last_error). */
+tm_status tm_motif_specialise(tm_motif *mo);
+
 /* Whether the motif runs on a compile-time specialised kernel (1) or on the
  * generic kernel with a runtime plan (0). */
 tm_status tm_motif_specialised(const tm_motif *mo, int *specialised);

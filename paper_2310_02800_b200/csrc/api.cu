@@ -278,22 +278,35 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         }
         if (p.n_roots > 0) {
             bool spec = false;
-            KernelInfo ki = lookup_kernel(mo->code, mode, &spec, mo->constrained());
-            const size_t smem = (size_t)ki.smem_per_warp * kWarpsPerBlock;
+            // a runtime-specialised kernel (tm_motif_specialise) first, then the
+            // build-time catalog, then the generic kernel
+            void *rfn = (mode == kCount || mode == kEnum) ? mo->rtc_fn[mode] : nullptr;
+            KernelInfo ki{nullptr, 0};
+            if (!rfn) ki = lookup_kernel(mo->code, mode, &spec, mo->constrained());
+            const size_t smem = (size_t)(rfn ? mo->rtc_smem[mode] : ki.smem_per_warp) * kWarpsPerBlock;
             {
                 std::lock_guard<std::mutex> lk(g_attr_mu);
-                auto key = (const void *)ki.fn;
+                auto key = rfn ? (const void *)rfn : (const void *)ki.fn;
                 if (!g_attr_done.count(key)) {
-                    TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    if (rfn) {
+                        TM_CUDA_TRY(rtc_set_smem(rfn, (int)smem));
+                    } else {
+                        TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)smem));
 #ifdef TM_CARVEOUT_MAX
-                    TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                                     (int)cudaSharedmemCarveoutMaxShared));
+                        TM_CUDA_TRY(cudaFuncSetAttribute(ki.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                         (int)cudaSharedmemCarveoutMaxShared));
 #endif
+                    }
                     g_attr_done[key] = 1;
                 }
             }
             int per_sm = 0;
-            TM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ki.fn, threads, smem));
+            if (rfn) {
+                TM_CUDA_TRY(rtc_occupancy(rfn, threads, smem, &per_sm));
+            } else {
+                TM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ki.fn, threads, smem));
+            }
             if (per_sm < 1) return fail(TM_ECUDA, "mining kernel does not fit on an SM");
             uint64_t grid = o.grid_ctas ? o.grid_ctas : (uint64_t)sms * per_sm;
             // no more warps than 32-root batches
@@ -324,7 +337,11 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             cfg.dynamicSmemBytes = smem;
             cfg.stream = s;
             cfg.numAttrs = 0;
-            TM_CUDA_TRY(cudaLaunchKernelEx(&cfg, ki.fn, p));
+            if (rfn) {
+                TM_CUDA_TRY(rtc_launch(rfn, (unsigned)grid, threads, smem, s, p));
+            } else {
+                TM_CUDA_TRY(cudaLaunchKernelEx(&cfg, ki.fn, p));
+            }
             g_info.launches++;
             g_info.grid_ctas = (uint32_t)grid;
             g_info.block_threads = threads;
@@ -510,6 +527,7 @@ tm_status tm_motif_set_vertex_label(tm_motif *mo, uint32_t vertex, int32_t label
     if (!mo || vertex >= 64 || mo->internal[vertex] < 0) return fail(TM_EINVAL, "vertex is not in the motif");
     if (label < TM_ANY_LABEL) return fail(TM_EINVAL, "label < -1");
     mo->vreq[mo->internal[vertex]] = label;
+    mo->rtc_fn[0] = mo->rtc_fn[1] = nullptr;   // a specialisation no longer fits: re-run tm_motif_specialise
     return TM_OK;
 }
 
@@ -518,6 +536,7 @@ tm_status tm_motif_set_edge_label(tm_motif *mo, uint32_t edge, int32_t label) {
     if (!mo || edge >= mo->L) return fail(TM_EINVAL, "edge >= L");
     if (label < TM_ANY_LABEL) return fail(TM_EINVAL, "label < -1");
     mo->ereq[edge] = label;
+    mo->rtc_fn[0] = mo->rtc_fn[1] = nullptr;
     return TM_OK;
 }
 
@@ -534,6 +553,7 @@ tm_status tm_motif_add_anti_edge(tm_motif *mo, uint32_t u, uint32_t v, uint32_t 
     mo->anti_v[j] = (uint8_t)mo->internal[v];
     mo->anti_attach[j] = (uint8_t)attach;
     mo->anti_window[j] = window;
+    mo->rtc_fn[0] = mo->rtc_fn[1] = nullptr;
     return TM_OK;
 }
 
@@ -546,7 +566,21 @@ tm_status tm_graph_set_labels(tm_graph *g, const int32_t *vlabels, const int32_t
 
 tm_status tm_motif_specialised(const tm_motif *mo, int *sp) {
     if (!mo || !sp) return fail(TM_EINVAL, "null argument");
-    *sp = is_specialised(mo->code) ? 1 : 0;
+    *sp = mo->rtc_fn[kCount] || (is_specialised(mo->code) && !mo->constrained()) ? 1 : 0;
+    return TM_OK;
+}
+
+tm_status tm_motif_specialise(tm_motif *mo) {
+    g_err.clear();
+    if (!mo) return fail(TM_EINVAL, "null motif");
+    if (is_specialised(mo->code) && !mo->constrained()) return TM_OK;   // in the build-time catalog
+    for (int mode : {(int)kCount, (int)kEnum}) {
+        RtcKernel k;
+        const tm_status st = rtc_kernel(mo->code, mo->constrained(), mode, &k);
+        if (st) return st;
+        mo->rtc_fn[mode] = k.fn;
+        mo->rtc_smem[mode] = k.smem_per_warp;
+    }
     return TM_OK;
 }
 

@@ -22,8 +22,6 @@
 // every stack within kCap = 64 tasks.
 #pragma once
 
-#include <utility>
-
 #include "tm_internal.cuh"
 
 namespace tmg {
@@ -76,15 +74,28 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return r;
 }
 
-// Compile-time loop: f(std::integral_constant<int, I>) for I = 0..N-1, so
-// that per-index layout decisions are constant expressions (if constexpr).
+// Compile-time loop: f(ic<I>) for I = 0..N-1, so that per-index layout
+// decisions are constant expressions (if constexpr).  Own index sequence:
+// the header also compiles under NVRTC (tm_motif_specialise), without <utility>.
+template <int V>
+struct ic {
+    static constexpr int value = V;
+};
+template <int... I>
+struct iseq {};
+template <int N, int... I>
+struct make_iseq : make_iseq<N - 1, N - 1, I...> {};
+template <int... I>
+struct make_iseq<0, I...> {
+    using type = iseq<I...>;
+};
 template <class F, int... I>
-__device__ __forceinline__ void sfor_impl(F &&f, std::integer_sequence<int, I...>) {
-    (f(std::integral_constant<int, I>{}), ...);
+__device__ __forceinline__ void sfor_impl(F &&f, iseq<I...>) {
+    (f(ic<I>{}), ...);
 }
 template <int N, class F>
 __device__ __forceinline__ void sfor(F &&f) {
-    if constexpr (N > 0) sfor_impl(f, std::make_integer_sequence<int, N>{});
+    if constexpr (N > 0) sfor_impl(f, typename make_iseq<N>::type{});
 }
 
 // First position p in [b, e) whose record's edge id is > key (e if none):
@@ -274,14 +285,20 @@ __host__ __device__ constexpr Shape shape_of() {
 // per-level choice (which list, which checks, how many mapped vertices, the
 // anchor) is a constant — the B200 counterpart of the paper's generated
 // motif-specific code.
-template <uint64_t CODE>
+// GEN: the generalized query (labels, anti-edges) is checked too; tasks then
+// keep every φ slot and matched id (a complete match's anti-edge check reads
+// them).  Catalog kernels are GEN = false; GEN = true ones are compiled at run
+// time (tm_motif_specialise, csrc/rtc.cu).
+template <uint64_t CODE, bool GEN = false>
 struct PlanC {
-    static constexpr bool kGeneral = false;   // labels / anti-edges: generic plan only
+    static constexpr bool kGeneral = GEN;
     static constexpr int kL = shape_of<CODE>().L;
     // φ slots stored with a level-l task
     __host__ __device__ static constexpr int nslots(int l) { return shape_of<CODE>().nv(l); }
-    __host__ __device__ static constexpr bool keep_phi(int l, int k) { return shape_of<CODE>().keep_phi(l, k); }
-    __host__ __device__ static constexpr bool keep_eh(int l, int k) { return shape_of<CODE>().keep_eh(l, k); }
+    __host__ __device__ static constexpr bool keep_phi(int l, int k) {
+        return GEN ? k < nslots(l) : shape_of<CODE>().keep_phi(l, k);
+    }
+    __host__ __device__ static constexpr bool keep_eh(int l, int k) { return GEN || shape_of<CODE>().keep_eh(l, k); }
     __host__ __device__ static constexpr bool keep_hi(int l) { return shape_of<CODE>().keep_hi(l); }
     __device__ explicit PlanC(const MineParams &) {}
     // every accessor is forced through a constant expression, so no decode
@@ -1015,7 +1032,7 @@ struct MinBlocks {
     static constexpr int value = 1;
 };
 template <uint64_t CODE>
-struct MinBlocks<PlanC<CODE>, kCount> {
+struct MinBlocks<PlanC<CODE, false>, kCount> {
     static constexpr int value = PlanC<CODE>::kL <= 3 ? TM_MIN_BLOCKS3 : PlanC<CODE>::kL == 4 ? TM_MIN_BLOCKS4 : TM_MIN_BLOCKS5;
 };
 
@@ -1144,9 +1161,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (MinBlocks<Plan, MODE>::v
     }
 }
 
+#ifndef __CUDACC_RTC__
 template <class Plan, int MODE>
 KernelInfo kernel_info() {
     return KernelInfo{&mine_kernel<Plan, MODE>, (int)(Layout<Plan, MODE>::warp_words() * sizeof(uint32_t))};
 }
+#endif
 
 }  // namespace tmg

@@ -1,9 +1,20 @@
 // Internal declarations of libtmotif (not part of the ABI).
 #pragma once
 
+#ifdef __CUDACC_RTC__
+// NVRTC (tm_motif_specialise compiles mine.cuh at run time): no host headers
+typedef unsigned char uint8_t;
+typedef signed char int8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#define INT64_MAX 9223372036854775807LL
+#else
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <string>
+#endif
 
 #include "../../include/tmotif.h"
 
@@ -118,6 +129,7 @@ __device__ __forceinline__ bool pair_maybe(const uint32_t *bits, uint32_t fmask,
 
 }  // namespace tmg
 
+#ifndef __CUDACC_RTC__
 struct tm_graph {
     int device = 0;
     tmg::DeviceGraph d;
@@ -137,6 +149,8 @@ struct tm_motif {
     uint32_t n_anti = 0;
     uint8_t anti_u[TM_MAX_ANTI] = {}, anti_v[TM_MAX_ANTI] = {}, anti_attach[TM_MAX_ANTI] = {};
     int64_t anti_window[TM_MAX_ANTI] = {};
+    void *rtc_fn[2] = {nullptr, nullptr};   // tm_motif_specialise: count / enumerate kernels (CUfunction)
+    int rtc_smem[2] = {0, 0};               // their shared memory per warp (bytes)
     bool constrained() const {
         if (n_anti) return true;
         for (uint32_t i = 0; i < nv; i++) if (vreq[i] != TM_ANY_LABEL) return true;
@@ -144,6 +158,7 @@ struct tm_motif {
         return false;
     }
 };
+#endif  // !__CUDACC_RTC__
 
 namespace tmg {
 
@@ -227,6 +242,8 @@ struct CensusParams {
     uint64_t root_lo, n_roots;
     unsigned long long *counts;     // 36 bins, index a * 6 + b
 };
+
+#ifndef __CUDACC_RTC__
 cudaError_t launch_census36(const CensusParams &p, int grid, cudaStream_t s);
 
 using MineKernel = void (*)(MineParams);
@@ -235,6 +252,17 @@ struct KernelInfo {
     MineKernel fn;
     int smem_per_warp;    // bytes
 };
+
+// Runtime-specialised kernels (csrc/rtc.cu, tm_motif_specialise): a CUfunction
+// of mine_kernel<PlanC<code, gen>, mode> compiled with NVRTC, and its launch.
+struct RtcKernel {
+    void *fn = nullptr;     // CUfunction
+    int smem_per_warp = 0;  // bytes
+};
+tm_status rtc_kernel(uint64_t code, bool gen, int mode, RtcKernel *out);
+cudaError_t rtc_set_smem(void *fn, int bytes);
+cudaError_t rtc_occupancy(void *fn, int threads, size_t smem, int *per_sm);
+cudaError_t rtc_launch(void *fn, unsigned grid, int threads, size_t smem, cudaStream_t s, const MineParams &p);
 
 // catalog lookup: specialised kernel for `code` in `mode`, else the generic one
 KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised, bool generic = false);
@@ -249,9 +277,11 @@ void dev_free(void *p, cudaStream_t s);
 // error plumbing
 void set_error(const std::string &msg);
 tm_status fail(tm_status st, const std::string &msg);
+#endif  // !__CUDACC_RTC__
 
 }  // namespace tmg
 
+#ifndef __CUDACC_RTC__
 #define TM_CUDA_TRY(expr)                                                                   \
     do {                                                                                     \
         cudaError_t _e = (expr);                                                             \
@@ -259,3 +289,4 @@ tm_status fail(tm_status st, const std::string &msg);
             return tmg::fail(_e == cudaErrorMemoryAllocation ? TM_ENOMEM : TM_ECUDA,          \
                             std::string(#expr) + ": " + cudaGetErrorString(_e));             \
     } while (0)
+#endif  // !__CUDACC_RTC__

@@ -77,6 +77,7 @@ SIGNATURES = [
     ("tm_motif_set_edge_label", _i32, [_P, _u32, _i32]),
     ("tm_motif_add_anti_edge", _i32, [_P, _u32, _u32, _u32, _i64]),
     ("tm_motif_specialised", _i32, [_P, ctypes.POINTER(_i32)]),
+    ("tm_motif_specialise", _i32, [_P]),
     ("tm_run_opts_default", None, [ctypes.POINTER(RunOpts)]),
     ("tm_count", _i32, [_P, _P, ctypes.POINTER(RunOpts), ctypes.POINTER(_u64)]),
     ("tm_enumerate", _i32, [_P, _P, ctypes.POINTER(RunOpts), _P, _u64, ctypes.POINTER(_u64),
@@ -267,6 +268,11 @@ class Motif:
         s = _i32()
         _check(lib().tm_motif_specialised(self._h, ctypes.byref(s)))
         return bool(s.value)
+
+    def specialise(self):
+        """Compile this motif's own kernels with NVRTC (tm_motif_specialise)."""
+        _check(lib().tm_motif_specialise(self._h))
+        return self
 
     def close(self):
         if getattr(self, "_h", None) and _lib is not None:

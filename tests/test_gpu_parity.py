@@ -526,3 +526,38 @@ def test_generalized_query_errors():
         T.Motif(M.P3, 10, elabels=[0, 0, 0, 0])
     with pytest.raises(ValueError):
         g.set_labels([0, 1])
+
+
+# ------------------------------------- runtime-specialised kernels (N3, NVRTC)
+def test_runtime_specialisation_parity():
+    """tm_motif_specialise compiles the kernel template for motifs outside the
+    build-time catalog (and GEN variants for labels / anti-edges); results stay
+    bit-exact against the oracle and the generic kernel."""
+    src, dst, t, n = synth.config_graph("C3", m=300_000)
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    rng = np.random.default_rng(9)
+    vlab = rng.integers(0, 2, n).astype(np.int32)
+    og.set_labels(vlab, None)
+    g.set_labels(vlab, None)
+    day = 86400
+    cases = [([(0, 1), (1, 2), (2, 3), (0, 3)], day, None, {}),               # not in the catalog
+             ([(0, 1), (0, 2), (2, 1), (1, 3)], day, [7200, None, 3600], {}),
+             ([(0, 1), (1, 0), (0, 2)], 3600, None, {}),                        # a P36 motif (catalog)
+             (M.C4, day, [21600] * 3, {"vlabels": {0: 1}, "anti": [(2, 0, 2, 3600)]}),   # catalog + constraints
+             (M.TRI, day, None, {"elabels": None, "anti": [(1, 0, 0, 600)]})]
+    for mot, d, f, cons in cases:
+        exp = og.mine(mot, d, f, enumerate_=True, **cons)
+        generic = T.Motif(mot, d, f, **cons)
+        c_generic = T.tm_count(g, generic)
+        mo = T.Motif(mot, d, f, **cons).specialise()
+        assert mo.specialised
+        assert T.tm_count(g, mo) == c_generic == exp["count"], (mot, cons)
+        rows, n_total = gpu_rows(g, mo)
+        assert n_total == exp["n_total"]
+        assert rows == [tuple(int(x) for x in r) for r in exp["rows"]]
+    # changing a constraint drops the specialisation (the kernel would not check it)
+    mo = T.Motif([(0, 1), (1, 2), (2, 3), (0, 3)], day).specialise()
+    assert mo.specialised
+    T.lib().tm_motif_add_anti_edge(mo.handle, 3, 1, 0, 100)
+    assert not mo.specialised
