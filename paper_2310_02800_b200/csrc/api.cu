@@ -18,7 +18,8 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
                        const tm_graph_opts *o, tm_graph **out);
 void graph_destroy(tm_graph *g);
 cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, uint64_t *scratch, cudaStream_t s);
-cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s);
+cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s,
+                        uint4 *W = nullptr);
 cudaError_t build_tie_lo(const DeviceGraph &d, uint32_t *S, cudaStream_t s);
 tm_status set_labels(DeviceGraph &d, const int32_t *vl, const int32_t *el, bool on_device);
 size_t horizon_scratch_words(uint64_t m);
@@ -211,8 +212,9 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         TM_CUDA_TRY(dev_alloc((void **)&hscr, horizon_scratch_words(m) * sizeof(uint64_t), s));
         fr.v.push_back(hscr);
     }
+    const size_t hr_elem = TM_HRANK == 3 ? sizeof(uint4) : sizeof(uint32_t);
     if (!hkeys.empty()) {
-        TM_CUDA_TRY(dev_alloc((void **)&hrbuf, hkeys.size() * m * sizeof(uint32_t), s));
+        TM_CUDA_TRY(dev_alloc((void **)&hrbuf, hkeys.size() * m * hr_elem, s));
         fr.v.push_back(hrbuf);
     }
     uint32_t *tie = nullptr;
@@ -235,7 +237,12 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             TM_CUDA_TRY(cudaMemsetAsync(hrbuf, 0, hkeys.size() * m * sizeof(uint32_t), s));
         } else {
             for (size_t i = 0; i < hkeys.size(); i++) {
-                TM_CUDA_TRY(build_hrank(d, hkeys[i].first, hbuf + (size_t)hkeys[i].second * m, hrbuf + i * m, s));
+                uint32_t *Hh = hbuf + (size_t)hkeys[i].second * m;
+                if (TM_HRANK == 3) {
+                    TM_CUDA_TRY(build_hrank(d, hkeys[i].first, Hh, nullptr, s, (uint4 *)hrbuf + i * m));
+                } else {
+                    TM_CUDA_TRY(build_hrank(d, hkeys[i].first, Hh, hrbuf + i * m, s));
+                }
                 g_info.launches++;
             }
         }
@@ -273,7 +280,10 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             p.H = hbuf + (size_t)dl[i] * m;
             for (uint32_t j = 0; j + 1 < mo->L; j++) {
                 p.Hf[j] = gap[i][j] >= 0 ? hbuf + (size_t)gap[i][j] * m : nullptr;
-                p.HR[j] = hwhich[i][j] >= 0 ? hrbuf + (size_t)hwhich[i][j] * m : nullptr;
+                if (TM_HRANK == 3)
+                    p.HW[j] = hwhich[i][j] >= 0 ? (const uint4 *)hrbuf + (size_t)hwhich[i][j] * m : nullptr;
+                else
+                    p.HR[j] = hwhich[i][j] >= 0 ? hrbuf + (size_t)hwhich[i][j] * m : nullptr;
             }
         }
         if (p.n_roots > 0) {

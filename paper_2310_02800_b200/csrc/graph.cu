@@ -383,9 +383,12 @@ __device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, co
 
 constexpr int kHrUnroll = 4;   // edges per thread in flight (independent load chains)
 
+// R: window-end ranks (u32 per edge), or W: window descriptors {start, end,
+// H[e], 0} (uint4 per edge) when W != nullptr
 __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ rank,
                                                const uint32_t *__restrict__ vtx, const uint32_t *__restrict__ offs,
-                                               const uint32_t *__restrict__ H, uint64_t m, uint32_t *__restrict__ R) {
+                                               const uint32_t *__restrict__ H, uint64_t m, uint32_t *__restrict__ R,
+                                               uint4 *__restrict__ W) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < m; e0 += stride * kHrUnroll) {
         uint32_t lim[kHrUnroll], b[kHrUnroll];
@@ -416,7 +419,8 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
             for (int k = 3; k >= 0; --k)
                 if (a + k >= b[u] && id[k] > lim[u]) ans = a + k;
             if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, vtx, offs, e, a + 4, lim[u]);
-            R[e] = ans;
+            if (W) W[e] = make_uint4(b[u], ans, lim[u], 0u);
+            else R[e] = ans;
         }
     }
 }
@@ -479,10 +483,11 @@ tm_status set_labels(DeviceGraph &d, const int32_t *vl, const int32_t *el, bool 
     return TM_OK;
 }
 
-cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s) {
+cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s,
+                        uint4 *W) {
     if (!d.m) return cudaSuccess;
     k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, d.rank + (size_t)var * d.m, var < 2 ? d.src : d.dst,
-                                          (var & 1) ? d.off_in : d.off_out, H, d.m, R);
+                                          (var & 1) ? d.off_in : d.off_out, H, d.m, R, W);
     return cudaGetLastError();
 }
 

@@ -43,9 +43,11 @@ constexpr int kRootChunk = 128;      // roots claimed per global atomic
 #endif
 constexpr int kShareMin = TM_SHARE_MIN;   // smallest window handed to an idle warp (share = 0)
 #ifndef TM_HRANK
-#define TM_HRANK 1          // window-end ranks: 0 off, 1 precomputed per query (build_hrank), 2 memoised in-kernel
+#define TM_HRANK 3          // window-end ranks: 0 off, 1 precomputed per query (build_hrank), 2 memoised in-kernel,
+                            // 3 precomputed window descriptors {start, end, H_δi} (one 16-byte load)
 #endif
 constexpr bool kHrankMemo = TM_HRANK == 2;
+constexpr bool kHrankDesc = TM_HRANK == 3;
 #ifndef TM_SHARE_POLL
 #define TM_SHARE_POLL 16
 #endif
@@ -550,8 +552,15 @@ struct Warp {
             const uint32_t *hf = p.Hf[NL - 1];
             uint32_t lim = hi;   // min(t_root + δ, t_prev + δ_i) as an id; H_δi read when needed
             uint32_t hfv = ~0u;
+            // window descriptor of e: {window start, window end, H_δi[e]} in one load
+            const uint4 *hw = nullptr;
+            if constexpr (kHrankDesc && MODE != kStats)
+                if (plan.template anc<NL>() == NL - 1 && !plan.template pairk<NL>()) hw = p.HW[NL - 1];
+            uint4 w4 = make_uint4(0u, 0u, ~0u, 0u);
+            if (hw) w4 = __ldg(hw + e);
             if (MODE == kStats || !plan.template pairk<NL>()) {
-                if (hf) hfv = __ldg(hf + e);
+                if (hw) hfv = w4.z;
+                else if (hf) hfv = __ldg(hf + e);
                 lim = min(hi, hfv);
             }
             if (MODE == kStats) {
@@ -611,10 +620,15 @@ struct Warp {
                 // load, issued with the start and H_δi loads (no record reads)
                 uint32_t *hr = (j == NL - 1) ? p.HR[NL - 1] : nullptr;
                 uint32_t hrv = 0;
-                if (hr) hrv = kHrankMemo ? __ldcg(hr + e) : __ldg(hr + e);   // the memo is written by this kernel
-                lo = __ldg(p.rank + (size_t)var * p.m + ea);
-                if (j != NL - 1) lo = scan_after(p.rec, lo, e);
-                const bool fine_binds = hr && hfv <= hi;            // lim == H_δi[e]: the end depends on e only
+                if (hw) {
+                    lo = w4.x;
+                    hrv = w4.y;
+                } else {
+                    if (hr) hrv = kHrankMemo ? __ldcg(hr + e) : __ldg(hr + e);   // the memo is written by this kernel
+                    lo = __ldg(p.rank + (size_t)var * p.m + ea);
+                    if (j != NL - 1) lo = scan_after(p.rec, lo, e);
+                }
+                const bool fine_binds = (hw || hr) && hfv <= hi;   // lim == H_δi[e]: the end depends on e only
                 const bool known = fine_binds && (!kHrankMemo || hrv != 0);
                 const uint32_t up_known = kHrankMemo ? hrv - 1 : hrv;
                 uint32_t pp = lo;

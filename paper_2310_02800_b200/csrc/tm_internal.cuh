@@ -188,6 +188,7 @@ struct MineParams {
     uint32_t fmask;
     const uint32_t *H;                 // H_δ  (coarse δ-horizon)
     const uint32_t *Hf[kMaxL];         // H_{δ_i} per gap i, nullptr when δ_i = ∞
+    const uint4 *HW[kMaxL];            // per gap i (TM_HRANK == 3): window descriptors {start, end, H_δi, 0}
     uint32_t *HR[kMaxL];               // per gap i: window-end ranks of H_{δ_i} in the list motif edge
                                        // i+1 reads (build_hrank, or a zeroed memo of pos + 1 the kernel
                                        // fills, TM_HRANK == 2), nullptr when not applicable
