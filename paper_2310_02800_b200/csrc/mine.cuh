@@ -1049,6 +1049,13 @@ template <uint64_t CODE>
 struct MinBlocks<PlanC<CODE, false>, kCount> {
     static constexpr int value = PlanC<CODE>::kL <= 3 ? TM_MIN_BLOCKS3 : PlanC<CODE>::kL == 4 ? TM_MIN_BLOCKS4 : TM_MIN_BLOCKS5;
 };
+#ifndef TM_MIN_BLOCKS_ENUM
+#define TM_MIN_BLOCKS_ENUM 4
+#endif
+template <uint64_t CODE>
+struct MinBlocks<PlanC<CODE, false>, kEnum> {
+    static constexpr int value = TM_MIN_BLOCKS_ENUM;
+};
 
 template <class Plan, int MODE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, (MinBlocks<Plan, MODE>::value)) mine_kernel(const MineParams p) {
