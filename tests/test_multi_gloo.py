@@ -15,7 +15,9 @@ import oracle
 from paper_2310_02800_b200 import motifs as M
 from paper_2310_02800_b200 import multi, synth
 
-CASES = [("TRI", 3600, None), ("C4", 3600, [1800, 1800, 1800]), ("P3", 3600, [600, 600])]
+# (motif, δ, δ_i, anti-edges): an anti-edge window extends the halo (multi.reach)
+CASES = [("TRI", 3600, None, None), ("C4", 3600, [1800, 1800, 1800], None), ("P3", 3600, [600, 600], None),
+         ("TRI", 3600, None, [(1, 0, 2, 7200)]), ("P3", 1800, [600, 600], [(3, 0, 1, 3600), (0, 2, 0, 900)])]
 
 
 def _free_port():
@@ -34,11 +36,11 @@ def _worker(rank, world, port, out):
     order = np.lexsort((np.arange(len(t)), t))        # (t, input position): sorted edge ids
     S, D, Tt = src[order], dst[order], t[order]
     counts = []
-    for name, delta, fine in CASES:
+    for name, delta, fine, anti in CASES:
         mot = M.get(name)
-        lo, hi, ehi = multi.rank_slice(Tt, multi.reach(delta, fine), world, rank)
+        lo, hi, ehi = multi.rank_slice(Tt, multi.reach(delta, fine, anti), world, rank)
         g = oracle.Graph(S[lo:ehi], D[lo:ehi], Tt[lo:ehi], n)
-        counts.append(g.mine(mot, delta, fine, root_range=(0, hi - lo))["count"])
+        counts.append(g.mine(mot, delta, fine, root_range=(0, hi - lo), anti=anti)["count"])
     total = multi.allreduce_counts(counts)
     out[rank] = total
     dist.barrier()
@@ -59,7 +61,7 @@ def test_partitioned_counts_allreduce_to_global(world):
         assert p.exitcode == 0
     src, dst, t, n = synth.config_graph("C1")
     g = oracle.Graph(src, dst, t, n)
-    expect = [g.mine(M.get(name), delta, fine)["count"] for name, delta, fine in CASES]
+    expect = [g.mine(M.get(name), delta, fine, anti=anti)["count"] for name, delta, fine, anti in CASES]
     assert all(out[r] == expect for r in range(world))
     assert sum(expect) > 0
 
@@ -69,3 +71,4 @@ def test_reach():
     assert multi.reach(100, [30, 20]) == 50
     assert multi.reach(100, [80, 80]) == 100
     assert multi.reach(100, [None, 5]) == 100
+    assert multi.reach(100, [30, 20], [(0, 1, 0, 40), (1, 2, 1, 70)]) == 120
