@@ -641,8 +641,31 @@ struct Warp {
                 // to kLeafSectors sectors; non-leaf: one sector to size the window
                 // (none when the end is known)
                 int nsec = leaf ? kLeafSectors : (known ? 0 : 1);
-                if (leaf && known)   // only the sectors the window covers; an empty window reads nothing
-                    nsec = up_known <= lo ? 0 : min(kLeafSectors, (int)(((up_known - 1) >> 2) - (lo >> 2)) + 1);
+                if (leaf && known) {
+                    // the window [lo, up_known) is known: scan only the sectors it covers
+                    // (an empty window reads nothing), with no end test per record
+                    const int cover = up_known <= lo ? 0 : (int)(((up_known - 1) >> 2) - (lo >> 2)) + 1;
+                    const int ns = min(kLeafSectors, cover);
+                    uint32_t a4 = lo & ~3u;
+#pragma unroll 1
+                    for (int it = 0; it < ns; ++it, a4 += 4) {
+                        const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(p.rec + a4);
+                        const ulonglong2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
+                        const uint64_t r4[4] = {x0.x, x0.y, x1.x, x1.y};
+#pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            const uint32_t q = a4 + k;
+                            if (q >= lo && q < up_known && accept<NL>((uint32_t)r4[k], dir == 0, phi)) {
+                                cnt++;
+                                if (MODE == kEnum) emit_one<NE>(eh, e, (uint32_t)(r4[k] >> 32), NL);
+                            }
+                        }
+                    }
+                    done = ns == cover;   // fully scanned, else the remainder [a4, up_known) becomes a task
+                    pp = a4;
+                    up = up_known;
+                    nsec = 0;
+                }
 #pragma unroll 1
                 for (int it = 0; it < nsec && !done; ++it) {
                     const uint32_t a4 = pp & ~3u;

@@ -1,6 +1,8 @@
 """Per-source-line warp-stall attribution: joins the SASS stall samples of an
 .ncu-rep kernel with the -lineinfo line table of the same kernel's cubin.
-usage: python tools/sass_lines.py REP KERNEL_REGEX OBJ_FILE MANGLED_SUBSTR [N] [SKIP]"""
+usage: python tools/sass_lines.py REP KERNEL_REGEX OBJ_FILE MANGLED_SUBSTR [N] [SKIP] [COLUMN]
+COLUMN: a source-page column, default "Warp Stall Sampling (All Samples)"; e.g.
+"Instructions Executed" for where the warp instructions go."""
 import csv
 import io
 import os
@@ -19,10 +21,11 @@ lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
 rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
 hdr = rows[0]
-S = hdr.index("Warp Stall Sampling (All Samples)")
+COL = sys.argv[7] if len(sys.argv) > 7 else "Warp Stall Sampling (All Samples)"
+S = hdr.index(COL)
 data = [r for r in rows[1:] if r and r[0].startswith("0x")]
 base = int(data[0][0], 16)
-samples = [(int(r[0], 16) - base, float(r[S] or 0), r[1].strip()) for r in data]
+samples = [(int(r[0], 16) - base, float((r[S] or "0").replace(",", "")), r[1].strip()) for r in data]
 # line table
 td = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", obj], cwd=td, capture_output=True)
