@@ -665,6 +665,27 @@ struct Warp {
                     pp = a4;
                     up = up_known;
                     nsec = 0;
+                } else if (known && plan.template u<NL>() < plan.template nv<NL>() &&
+                           plan.template v<NL>() < plan.template nv<NL>()) {
+                    // inner closing edge (both endpoints mapped): few candidates
+                    // close (DIA's 2->0: ~1 in 800), so the window is pre-scanned here and
+                    // the task starts at its first closing candidate, or is not pushed
+                    const int cover = up_known <= lo ? 0 : (int)(((up_known - 1) >> 2) - (lo >> 2)) + 1;
+                    const int ns = min(kLeafSectors, cover);
+                    uint32_t a4 = lo & ~3u, first = 0xFFFFFFFFu;
+#pragma unroll 1
+                    for (int it = 0; it < ns && first == 0xFFFFFFFFu; ++it, a4 += 4) {
+                        const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(p.rec + a4);
+                        const ulonglong2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
+                        const uint64_t r4[4] = {x0.x, x0.y, x1.x, x1.y};
+#pragma unroll
+                        for (int k = 3; k >= 0; --k) {
+                            const uint32_t q = a4 + k;
+                            if (q >= lo && q < up_known && accept<NL>((uint32_t)r4[k], dir == 0, phi)) first = q;
+                        }
+                    }
+                    lo = first != 0xFFFFFFFFu ? first : (ns == cover ? up_known : a4);
+                    nsec = 0;
                 }
 #pragma unroll 1
                 for (int it = 0; it < nsec && !done; ++it) {
