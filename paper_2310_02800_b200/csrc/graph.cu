@@ -139,9 +139,14 @@ __global__ void k_outflag(const uint32_t *val, uint64_t n2, uint32_t *flag) {
 
 // off_out / off_in hold the sentinel-adjusted list starts (plain offset + v,
 // in-lists further shifted by m + n); the plain offsets are recovered here.
+// Records go to rec[] in place (consecutive incidences of a vertex are
+// consecutive positions); the two rank values of the incidence go to rk[i]
+// in incidence order and reach rank[] through a radix sort by incidence id
+// (k_rank_from_sorted): scattering them directly as 4-byte random writes
+// measured 12 ms of a 21 ms build on C4.
 __global__ void k_scatter_csr(const uint32_t *key, const uint32_t *val, const uint32_t *outb, const uint32_t *src,
                               const uint32_t *dst, const uint32_t *off_out, const uint32_t *off_in, uint64_t m,
-                              uint32_t n, uint64_t *rec, uint32_t *rank) {
+                              uint32_t n, uint64_t *rec, unsigned long long *rk) {
     const uint32_t split = (uint32_t)(m + n);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 2 * m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = key[i], ent = val[i], e = ent >> 1;
@@ -149,16 +154,34 @@ __global__ void k_scatter_csr(const uint32_t *key, const uint32_t *val, const ui
         const uint64_t seg = (uint64_t)(so - v) + (si - split - v);      // first incidence of v
         const uint32_t ob = outb[i] - outb[seg];                        // out-incidences of v before i
         const uint32_t ib = (uint32_t)(i - seg) - ob;                   // in-incidences of v before i
+        uint32_t a, b;
         if ((ent & 1u) == 0) {            // e in OUT(v), v = src(e)
             const uint32_t pos = so + ob;
-            rec[pos] = ((uint64_t)e << 32) | dst[e];
-            rank[e] = pos + 1;                                       // var 0: OUT(src e)
-            rank[m + e] = si + ib + (src[e] == dst[e] ? 1u : 0u);  // var 1: IN(src e), ids <= e
+            const uint32_t w = dst[e];
+            rec[pos] = ((uint64_t)e << 32) | w;
+            a = pos + 1;                          // var 0: OUT(src e)
+            b = si + ib + (v == w ? 1u : 0u);     // var 1: IN(src e), ids <= e
         } else {                          // e in IN(v), v = dst(e)
             const uint32_t pos = si + ib;
             rec[pos] = ((uint64_t)e << 32) | src[e];
-            rank[3 * m + e] = pos + 1;                               // var 3: IN(dst e)
-            rank[2 * m + e] = so + ob;                               // var 2: OUT(dst e), ids <= e
+            a = pos + 1;                          // var 3: IN(dst e)
+            b = so + ob;                          // var 2: OUT(dst e), ids <= e
+        }
+        rk[i] = ((unsigned long long)a << 32) | b;
+    }
+}
+
+// rk sorted by incidence id 2e + dir: the rank values of edge e, coalesced
+__global__ void k_rank_from_sorted(const unsigned long long *rk, uint64_t m, uint32_t *rank) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < 2 * m; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t e = j >> 1;
+        const unsigned long long v = rk[j];
+        if ((j & 1) == 0) {
+            rank[e] = (uint32_t)(v >> 32);         // var 0
+            rank[m + e] = (uint32_t)v;             // var 1
+        } else {
+            rank[3 * m + e] = (uint32_t)(v >> 32); // var 3
+            rank[2 * m + e] = (uint32_t)v;         // var 2
         }
     }
 }
@@ -244,12 +267,15 @@ cudaError_t build_csr(DeviceGraph &d, cudaStream_t s) {
     const uint64_t m = d.m;
     const uint32_t n = d.n;
     uint32_t *deg = nullptr, *key = nullptr, *val = nullptr, *kout = nullptr, *vout = nullptr, *flag = nullptr;
+    unsigned long long *rk = nullptr, *rk2 = nullptr;
     void *tmp = nullptr;
-    size_t sort_bytes = 0, scan_bytes = 0, scan2_bytes = 0;
+    size_t sort_bytes = 0, scan_bytes = 0, scan2_bytes = 0, sort2_bytes = 0;
     cudaError_t err;
     int end_bit = 1;
     while (end_bit < 32 && (1ull << end_bit) < (uint64_t)n) end_bit++;
     const uint64_t n2 = 2 * m;
+    int end_bit2 = 1;   // incidence ids 2e + dir < 2m
+    while (end_bit2 < 32 && (1ull << end_bit2) < n2) end_bit2++;
 #define TRY(x) do { err = (x); if (err != cudaSuccess) goto done; } while (0)
     TRY(dmalloc(&deg, 2 * ((size_t)n + 1), s));
     TRY(dmalloc(&key, n2 + 1, s));
@@ -260,7 +286,10 @@ cudaError_t build_csr(DeviceGraph &d, cudaStream_t s) {
     TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, key, kout, val, vout, (int64_t)n2, 0, end_bit, s));
     TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, deg, d.off_out, (int64_t)n + 1, s));
     TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan2_bytes, flag, key, (int64_t)n2 + 1, s));
-    TRY(dev_alloc(&tmp, std::max(sort_bytes, std::max(scan_bytes, scan2_bytes)), s));
+    TRY(dmalloc(&rk, n2, s));
+    TRY(dmalloc(&rk2, n2, s));
+    TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort2_bytes, vout, val, rk, rk2, (int64_t)n2, 0, end_bit2, s));
+    TRY(dev_alloc(&tmp, std::max(std::max(sort_bytes, sort2_bytes), std::max(scan_bytes, scan2_bytes)), s));
     TRY(cudaMemsetAsync(deg, 0, 2 * ((size_t)n + 1) * 4, s));
     if (m) {
         k_degree<<<grid_for(m), 256, 0, s>>>(d.src, m, deg);
@@ -277,13 +306,18 @@ cudaError_t build_csr(DeviceGraph &d, cudaStream_t s) {
         TRY(cudaMemsetAsync(flag + n2, 0, 4, s));
         TRY(cub::DeviceScan::ExclusiveSum(tmp, scan2_bytes, flag, key, (int64_t)n2 + 1, s));  // key: free after the sort
         k_scatter_csr<<<grid_for(n2), 256, 0, s>>>(kout, vout, key, d.src, d.dst, d.off_out, d.off_in, m, n,
-                                                   d.rec, d.rank);
+                                                   d.rec, rk);
+        // back to incidence order (val is free after the first sort)
+        TRY(cub::DeviceRadixSort::SortPairs(tmp, sort2_bytes, vout, val, rk, rk2, (int64_t)n2, 0, end_bit2, s));
+        k_rank_from_sorted<<<grid_for(n2), 256, 0, s>>>(rk2, m, d.rank);
     }
     TRY(cudaGetLastError());
     TRY(cudaStreamSynchronize(s));
 done:
 #undef TRY
-    for (void *q : {(void *)deg, (void *)key, (void *)val, (void *)kout, (void *)vout, (void *)flag, tmp}) dev_free(q, s);
+    for (void *q : {(void *)deg, (void *)key, (void *)val, (void *)kout, (void *)vout, (void *)flag, (void *)rk,
+                    (void *)rk2, tmp})
+        dev_free(q, s);
     return err;
 }
 
