@@ -301,6 +301,7 @@ def main():
     motifs = [T.Motif(*motif_fine(name)[:1], DELTA, motif_fine(name)[1]) for name in MOTIFS]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     balance = [None] * len(MOTIFS)   # load balance of the last step's mining kernels (§8 a8)
+    fused_into = [None] * len(MOTIFS)   # prefix fusion: the motif whose kernel counted this one
 
     def step(g, rr):
         if args.separate:   # one tm_count per motif, each building its own horizons
@@ -318,6 +319,7 @@ def main():
         kin = T.tm_last_kernel_info()
         for i, x in enumerate(kin):
             balance[i] = {"shared_tasks": x["shared_tasks"], "tail_ms": x["tail_ms"], "warp_busy": x["warp_busy"]}
+            fused_into[i] = MOTIFS[x["carried_by"]] if x["carried_by"] >= 0 else None
         return cs, [x["mine_ms"] for x in kin], T.tm_last_run_info()["launches"]
 
     def timed(fn):
@@ -361,6 +363,7 @@ def main():
                 _, (_, mm0, _) = timed(lambda: step(g, rr))
                 part0["mine_ms"] = mm0
                 part0["balance"] = [dict(x) for x in balance]
+                part0["fused_into"] = list(fused_into)
             g.close()
             del g
             # ---- end to end through the public API from pinned host memory
@@ -407,10 +410,13 @@ def main():
         bq = balgo_bytes(part0["stats"][i], part0["roots"], L, fine=FINE is not None)
         bytes_q.append(bq)
         ms = part0["mine_ms"][i]
-        per_motif.append({"motif": name, "count": counts[i], "mine_ms": ms,
-                          "alg_bytes": bq, "alg_GBps": bq / (ms / 1000) / 1e9,
+        fz = part0["fused_into"][i]
+        per_motif.append({"motif": name, "count": counts[i], "mine_ms": None if fz else ms,
+                          "alg_bytes": bq, "alg_GBps": None if fz else bq / (ms / 1000) / 1e9,
                           "search_nodes": sum(part0["stats"][i]["nodes"][1:L]),
-                          "window_sum": part0["stats"][i]["window_sum"], "load_balance": part0["balance"][i]})
+                          "window_sum": part0["stats"][i]["window_sum"],
+                          "load_balance": None if fz else part0["balance"][i],
+                          "counted_inside": fz})
     dom = int(np.argmax(part0["mine_ms"]))
     peak, peak_src = peaks()
     achieved = bytes_q[dom] / (part0["mine_ms"][dom] / 1000) / 1e9

@@ -178,6 +178,12 @@ typedef struct {
                              /* idle warps through a global ticket queue; 1 = off;   */
                              /* 2 = eager (also leaf-level tasks; a test mode).      */
                              /* Results are identical in every mode.                 */
+    int32_t fuse;            /* tm_count_multi: 0 = a motif that is the first l      */
+                             /* edges of another motif of the call (same δ and       */
+                             /* δ_1..δ_{l-1}, no labels / anti-edges) is counted     */
+                             /* inside that motif's kernel — its matches are the     */
+                             /* search-tree nodes at level l — instead of by its own */
+                             /* kernel; 1 = off.  Counts are identical.               */
 } tm_run_opts;
 
 /* Fill *o with the defaults above. */
@@ -242,6 +248,7 @@ typedef struct {
     float warp_busy;
     uint32_t grid_ctas;
     uint64_t shared_tasks;
+    int32_t carried_by;      /* prefix fusion: index of the motif whose kernel counted this one, else -1 */
 } tm_kernel_info;
 
 /* Copies min(cap, n) entries to out (host); *n = number of kernels. */

@@ -73,16 +73,17 @@ bool is_specialised(uint64_t code) {
 }
 
 KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised, bool generic) {
-    if (!generic && (mode == kCount || mode == kEnum)) {
+    if (!generic && (mode == kCount || mode == kEnum || mode == kCountPfx)) {
         for (auto &e : catalog())
-            if (e.code == code) {
+            if (e.code == code && (mode != kCountPfx || e.count_pfx.fn)) {
                 if (specialised) *specialised = true;
-                return mode == kCount ? e.count : e.enumerate;
+                return mode == kCount ? e.count : mode == kEnum ? e.enumerate : e.count_pfx;
             }
     }
     if (specialised) *specialised = false;
     switch (mode) {
         case kCount: return kernel_info<PlanR, kCount>();
+        case kCountPfx: return kernel_info<PlanR, kCountPfx>();
         case kEnum: return kernel_info<PlanR, kEnum>();
         case kRoots: return kernel_info<PlanR, kRoots>();
         default: return kernel_info<PlanR, kStats>();
@@ -186,6 +187,39 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         }
     }
 
+    // prefix fusion (counting): the longest motifs run their kernels; a motif
+    // that is the first l edges of one of them, with the same δ and effective
+    // δ_1..δ_{l-1} and no constraints, is counted there as its level-l nodes
+    std::vector<int> carrier(k, -1);
+    std::vector<uint32_t> pmask(k, 0);
+    if (mode == kCount && o.fuse == 0 && k > 1) {
+        std::vector<uint32_t> order(k);
+        for (uint32_t i = 0; i < k; i++) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return mos[a]->L > mos[b]->L; });
+        auto eff = [](const tm_motif *mo, uint32_t g) {
+            const int64_t f = mo->fine[g];
+            return (f == TM_DELTA_INF || f >= mo->delta) ? TM_DELTA_INF : f;
+        };
+        for (uint32_t a = 0; a < k; a++) {
+            const uint32_t i = order[a];
+            const tm_motif *mi = mos[i];
+            if (mi->constrained()) continue;
+            for (uint32_t b = 0; b < a && carrier[i] < 0; b++) {
+                const uint32_t j = order[b];
+                const tm_motif *mj = mos[j];
+                if (carrier[j] >= 0 || mj->constrained() || mj->rtc_fn[kCount] || mj->L <= mi->L ||
+                    mj->delta != mi->delta)
+                    continue;
+                if (motif_code((int)mi->L, mj->u, mj->v) != mi->code) continue;
+                bool same = true;
+                for (uint32_t g = 0; g + 1 < mi->L; g++) same &= eff(mi, g) == eff(mj, g);
+                if (!same) continue;
+                carrier[i] = (int)j;
+                pmask[j] |= 1u << mi->L;
+            }
+        }
+    }
+
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evd = nullptr;
     std::vector<cudaEvent_t> evk(k, nullptr);
     struct EvFree {
@@ -257,7 +291,12 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
     const int threads = kWarpsPerBlock * 32;
     for (uint32_t i = 0; i < k; i++) {
         const tm_motif *mo = mos[i];
+        if (carrier[i] >= 0) {   // counted inside its carrier's kernel
+            TM_CUDA_TRY(cudaEventRecord(evk[i], s));
+            continue;
+        }
         MineParams p = base;
+        p.prefix_mask = pmask[i];
         p.L = mo->L;
         for (uint32_t j = 0; j < mo->L; j++) { p.u[j] = mo->u[j]; p.v[j] = mo->v[j]; }
         p.scratch = scratch + (size_t)i * kScratchWords;
@@ -290,9 +329,10 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             bool spec = false;
             // a runtime-specialised kernel (tm_motif_specialise) first, then the
             // build-time catalog, then the generic kernel
-            void *rfn = (mode == kCount || mode == kEnum) ? mo->rtc_fn[mode] : nullptr;
+            const int kmode = (mode == kCount && p.prefix_mask) ? (int)kCountPfx : mode;
+            void *rfn = (kmode == kCount || kmode == kEnum) ? mo->rtc_fn[kmode] : nullptr;
             KernelInfo ki{nullptr, 0};
-            if (!rfn) ki = lookup_kernel(mo->code, mode, &spec, mo->constrained());
+            if (!rfn) ki = lookup_kernel(mo->code, kmode, &spec, mo->constrained());
             const size_t smem = (size_t)(rfn ? mo->rtc_smem[mode] : ki.smem_per_warp) * kWarpsPerBlock;
             {
                 std::lock_guard<std::mutex> lk(g_attr_mu);
@@ -382,6 +422,12 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
                                        ((double)(te - t0) * ki.grid_ctas * kWarpsPerBlock));
         }
         out[i].count = mode == kEnum ? h[2] : h[1];
+        ki.carried_by = carrier[i];
+        if (carrier[i] >= 0) {
+            out[i].count = host[(size_t)carrier[i] * kScratchWords + kPrefixBase + mos[i]->L];
+            ki = tm_kernel_info{};
+            ki.carried_by = carrier[i];
+        }
         for (int w = 0; w < kScratchWords; w++) out[i].stats[w] = h[w];
 #ifdef TM_PHASE_PROFILE
         fprintf(stderr, "[phase]");

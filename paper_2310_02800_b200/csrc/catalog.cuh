@@ -20,11 +20,14 @@ constexpr uint64_t mcode(int L, int a0, int b0, int a1 = 0, int b1 = 0, int a2 =
 struct CatalogEntry {
     uint64_t code;
     KernelInfo count, enumerate;
+    KernelInfo count_pfx;   // counting + prefix fusion (named motifs); fn == nullptr: not instantiated
 };
 
-template <uint64_t CODE>
+template <uint64_t CODE, bool PFX = false>
 CatalogEntry entry() {
-    return CatalogEntry{CODE, kernel_info<PlanC<CODE>, kCount>(), kernel_info<PlanC<CODE>, kEnum>()};
+    KernelInfo pfx{nullptr, 0};
+    if constexpr (PFX) pfx = kernel_info<PlanC<CODE>, kCountPfx>();
+    return CatalogEntry{CODE, kernel_info<PlanC<CODE>, kCount>(), kernel_info<PlanC<CODE>, kEnum>(), pfx};
 }
 
 void register_named(std::vector<CatalogEntry> &v);

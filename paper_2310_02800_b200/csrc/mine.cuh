@@ -70,6 +70,12 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
+// Per-warp shared counters of prefix-fusion matches (lane 0 adds; MineParams::prefix_mask)
+__device__ __forceinline__ unsigned long long *prefix_counters() {
+    __shared__ unsigned long long c[kWarpsPerBlock][kMaxL];
+    return c[threadIdx.x >> 5];
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -548,6 +554,10 @@ struct Warp {
     __device__ __forceinline__ void push(bool ok, uint32_t e, uint32_t hi, const uint32_t (&phi)[NS],
                                          const uint32_t (&eh)[NE], uint32_t rslot) {
         uint32_t lo = 0, up = 0;
+        if (MODE == kCountPfx && (p.prefix_mask >> NL) & 1u) {   // these nodes are the matches of the NL-edge prefix
+            const uint32_t c = __popc(__ballot_sync(kFull, ok));
+            if (lane == 0) prefix_counters()[NL] += c;
+        }
         if (ok) {
             const uint32_t *hf = p.Hf[NL - 1];
             uint32_t lim = hi;   // min(t_root + δ, t_prev + δ_i) as an id; H_δi read when needed
@@ -1093,6 +1103,8 @@ template <uint64_t CODE>
 struct MinBlocks<PlanC<CODE, false>, kCount> {
     static constexpr int value = PlanC<CODE>::kL <= 3 ? TM_MIN_BLOCKS3 : PlanC<CODE>::kL == 4 ? TM_MIN_BLOCKS4 : TM_MIN_BLOCKS5;
 };
+template <uint64_t CODE>
+struct MinBlocks<PlanC<CODE, false>, kCountPfx> : MinBlocks<PlanC<CODE, false>, kCount> {};
 #ifndef TM_MIN_BLOCKS_ENUM
 #define TM_MIN_BLOCKS_ENUM 4
 #endif
@@ -1108,6 +1120,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (MinBlocks<Plan, MODE>::v
     constexpr int LM = Plan::kL;
     uint32_t *ws = smem + warp * Layout<Plan, MODE>::warp_words();
     const Plan plan(p);
+    if (MODE == kCountPfx && lane < kMaxL) prefix_counters()[lane] = 0;
+    __syncwarp();
     Warp<Plan, MODE> W(p, plan, ws, lane);
     const int L = plan.L();
     uint32_t next = 0, end = 0;
@@ -1199,6 +1213,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (MinBlocks<Plan, MODE>::v
         atomicMax(p.scratch + kTimeExit, te);
         atomicAdd(p.scratch + kTimeBusy, (unsigned long long)((uint32_t)(te >> 6) - t_start) << 6);
     }
+    __syncwarp();
+    if (MODE == kCountPfx && lane < kMaxL && prefix_counters()[lane])
+        atomicAdd(p.scratch + kPrefixBase + lane, prefix_counters()[lane]);
     unsigned long long tot = W.leaf_count;
     for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(kFull, tot, d);
     tot += W.count;   // lane 0's batch count (other lanes hold 0)

@@ -163,7 +163,10 @@ struct tm_motif {
 namespace tmg {
 
 // Modes of the mining kernel.
-enum Mode : int { kCount = 0, kEnum = 1, kRoots = 2, kStats = 3 };
+// kCountPfx: counting that also counts the nodes of the levels in
+// MineParams::prefix_mask (prefix fusion, tm_count_multi) — a separate
+// instantiation, so the plain counting kernels carry none of that code.
+enum Mode : int { kCount = 0, kEnum = 1, kRoots = 2, kStats = 3, kCountPfx = 4 };
 
 // Packed motif structure: bits 0-2 L, then per edge i: u at 3+6i, v at 6+6i.
 constexpr uint64_t motif_code(int L, const uint8_t *u, const uint8_t *v) {
@@ -208,6 +211,10 @@ struct MineParams {
     uint32_t *qrec;
     uint32_t qmask;
     uint32_t total_warps;
+    // prefix fusion (tm_count_multi): bit l set -> count the search-tree nodes
+    // created at level l (= the matches of this motif's l-edge prefix) into
+    // scratch[kPrefixBase + l]
+    uint32_t prefix_mask;
     // generalized query (PlanR only, gen != 0): labels and anti-edges
     int gen;
     const int32_t *vlab, *elab;        // graph labels (nullptr = all 0)
@@ -230,6 +237,7 @@ constexpr int kTimeStart = 40, kTimeDrain = 41, kTimeExit = 42, kTimeBusy = 43, 
 // warps (an int in the low half), subtrees handed over
 constexpr int kShareTail = 3, kShareHead = 4, kShareIdle = 5, kShareDone = 6;
 constexpr int kShareWords = 32;   // u32 words per shared task record (fields + level in word 31)
+constexpr int kPrefixBase = 32;   // scratch[32 + l]: prefix matches (nodes created at level l)
 constexpr int kStatsBase = 8;   // scratch[8 + l] nodes[l], [16] window, [17] list, [18] probes, [19] fast window
 
 // Parameters of the fused 36-motif census (census.cu).

@@ -41,7 +41,7 @@ class GraphOpts(ctypes.Structure):
 class RunOpts(ctypes.Structure):
     _fields_ = [("stream", _P), ("root_lo", _u64), ("root_hi", _u64), ("edge_id_offset", _u64),
                 ("canonical", _i32), ("buffers_on_device", _i32), ("grid_ctas", _u32),
-                ("block_threads", _u32), ("share", _i32)]
+                ("block_threads", _u32), ("share", _i32), ("fuse", _i32)]
 
 
 class SearchStats(ctypes.Structure):
@@ -57,7 +57,7 @@ class RunInfo(ctypes.Structure):
 
 class KernelInfo(ctypes.Structure):
     _fields_ = [("mine_ms", _f32), ("tail_ms", _f32), ("warp_busy", _f32), ("grid_ctas", _u32),
-                ("shared_tasks", _u64)]
+                ("shared_tasks", _u64), ("carried_by", _i32)]
 
 
 _lib = None
@@ -142,8 +142,9 @@ def _stream_handle(stream):
 
 
 def run_opts(stream=None, root_range=None, edge_id_offset=0, canonical=False, buffers_on_device=False,
-             grid_ctas=0, share=0) -> RunOpts:
-    """share: heavy-subtree sharing, 0 on (default), 1 off, 2 eager (tm_run_opts)."""
+             grid_ctas=0, share=0, fuse=0) -> RunOpts:
+    """share: heavy-subtree sharing, 0 on (default), 1 off, 2 eager; fuse: prefix
+    fusion in tm_count_multi, 0 on (default), 1 off (tm_run_opts)."""
     o = RunOpts()
     lib().tm_run_opts_default(ctypes.byref(o))
     o.stream = _stream_handle(stream)
@@ -154,6 +155,7 @@ def run_opts(stream=None, root_range=None, edge_id_offset=0, canonical=False, bu
     o.buffers_on_device = int(bool(buffers_on_device))
     o.grid_ctas = int(grid_ctas)
     o.share = int(share)
+    o.fuse = int(fuse)
     return o
 
 
@@ -343,7 +345,7 @@ def tm_last_kernel_info() -> list:
     buf = (KernelInfo * max(1, n.value))()
     _check(lib().tm_last_kernel_info(buf, n.value, ctypes.byref(n)))
     return [{"mine_ms": b.mine_ms, "tail_ms": b.tail_ms, "warp_busy": b.warp_busy, "grid_ctas": b.grid_ctas,
-             "shared_tasks": b.shared_tasks} for b in buf[: n.value]]
+             "shared_tasks": b.shared_tasks, "carried_by": b.carried_by} for b in buf[: n.value]]
 
 
 def tm_census36(g: Graph, delta: int, fine=None, **opts) -> np.ndarray:

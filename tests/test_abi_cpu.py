@@ -89,11 +89,12 @@ def test_partition_plan_tiles_roots_and_covers_halo():
 
 def test_declared_struct_sizes_match_binding():
     # the ctypes mirrors must match the C layout (x86-64 SysV)
-    # stream, root_lo/hi/offset, canonical, on_device, grid, block, share + 4 B tail padding
+    # stream, root_lo/hi/offset, canonical, on_device, grid, block, share, fuse
     assert ctypes.sizeof(T.RunOpts) == 8 + 8 * 3 + 4 * 2 + 4 * 2 + 4 + 4
-    assert T.RunOpts.share.offset == 48
+    assert T.RunOpts.share.offset == 48 and T.RunOpts.fuse.offset == 52
     # 3 f32 + 3 u32, shared_tasks u64, tail_ms, warp_busy
     assert ctypes.sizeof(T.RunInfo) == 24 + 8 + 4 + 4
     assert T.RunInfo.shared_tasks.offset == 24
-    assert ctypes.sizeof(T.KernelInfo) == 24 and T.KernelInfo.shared_tasks.offset == 16
+    assert ctypes.sizeof(T.KernelInfo) == 32 and T.KernelInfo.shared_tasks.offset == 16
+    assert T.KernelInfo.carried_by.offset == 24
     assert ctypes.sizeof(T.SearchStats) == 8 * 13

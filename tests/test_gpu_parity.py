@@ -561,3 +561,28 @@ def test_runtime_specialisation_parity():
     assert mo.specialised
     T.lib().tm_motif_add_anti_edge(mo.handle, 3, 1, 0, 100)
     assert not mo.specialised
+
+
+def test_prefix_fusion():
+    """tm_count_multi counts a motif that is a prefix of another (same δ and
+    gap bounds, no constraints) as that motif's level-l search-tree nodes:
+    P3 inside C4, TRI inside DIA and TT, PATH2 inside everything — counts equal
+    the unfused query and the oracle; a different δ_i or δ blocks the fusion."""
+    src, dst, t, n = synth.config_graph("C3", m=300_000)
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    d, f = 86400, 21600
+    specs = [("P3", d, [f] * 2), ("C4", d, [f] * 3), ("TRI", d, [f] * 2), ("DIA", d, [f] * 4),
+             ("TT", d, [f] * 3), ("PATH2", d, [f]), ("P3", d, [f, 3600]), ("TRI", 3600, [f] * 2),
+             ("TRI", d, None), ("TT", d, None)]
+    mos = [T.Motif(M.get(nm), dd, ff) for nm, dd, ff in specs]
+    fused = T.tm_count_multi(g, mos)
+    kin = T.tm_last_kernel_info()
+    plain = T.tm_count_multi(g, mos, fuse=1)
+    exp = [og.mine(M.get(nm), dd, ff)["count"] for nm, dd, ff in specs]
+    assert fused == plain == exp
+    carried = {i: x["carried_by"] for i, x in enumerate(kin) if x["carried_by"] >= 0}
+    # P3/d/f in C4, TRI/d/f in DIA, PATH2 in a longer motif, TRI/d/None in TT/d/None
+    assert set(carried) == {0, 2, 5, 8}, carried
+    assert carried[0] == 1 and carried[2] == 3 and carried[8] == 9
+    assert all(kin[i]["grid_ctas"] == 0 for i in carried)
