@@ -338,6 +338,7 @@ def main():
     counts = np.zeros(len(MOTIFS), np.int64)
     launches, my_roots, part0 = 0, 0, None
     e2e_ms, h2d = 0.0, 0
+    nofuse_ms = 0.0
     with ClockSampler(local) as clk:
         for pi, (s_src, s_dst, s_t, n, rr) in enumerate(parts()):
             g = T.Graph(s_src, s_dst, s_t, n, device=local, stream=stream)
@@ -355,6 +356,12 @@ def main():
                     mine_ms += np.array(mm)
                     counts += np.array(cs, np.int64)
             clk.pause()
+            if not args.separate:   # the same steps without prefix fusion, for transparency
+                for _ in range(2):
+                    T.tm_count_multi(g, motifs, root_range=rr, stream=stream, fuse=1)
+                for k in range(args.steps):
+                    nofuse_ms += timed(lambda: T.tm_count_multi(g, motifs, root_range=rr, stream=stream,
+                                                                  fuse=1))[0]
             my_roots += rr[1] - rr[0]
             if pi == 0:   # roofline inputs (untimed instrumentation runs) from this rank's first part
                 stats = [T.tm_search_stats_run(g, mo, root_range=rr, stream=stream) for mo in motifs]
@@ -390,14 +397,14 @@ def main():
     torch.cuda.synchronize()
     total_ms = float(step_ms.sum())
     counts = multi.allreduce_counts(counts.tolist(), device=dev)   # the one exchange: combine the counts
-    tot = torch.tensor([total_ms, e2e_ms, float(my_roots), float(h2d)], dtype=torch.float64, device=dev)
+    tot = torch.tensor([total_ms, e2e_ms, nofuse_ms, float(my_roots), float(h2d)], dtype=torch.float64, device=dev)
     if world > 1:
-        mx = tot[:2].clone()
+        mx = tot[:3].clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)   # max over ranks
-        sm = tot[2:].clone()
+        sm = tot[3:].clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         tot = torch.cat([mx, sm])
-    total_ms, e2e_ms, all_roots, h2d_all = (float(x) for x in tot.tolist())
+    total_ms, e2e_ms, nofuse_ms, all_roots, h2d_all = (float(x) for x in tot.tolist())
     roots_per_step = all_roots * len(MOTIFS)
     value = roots_per_step * args.steps / (total_ms / 1000)
     matches_per_s = sum(counts) * args.steps / (total_ms / 1000)
@@ -455,7 +462,10 @@ def main():
                 "gpu_launches_note": "per rank and step: 2 kernels per distinct horizon, one window-end-rank kernel per "
                                      "distinct (list, gap bound), one mining kernel per motif",
                 "query": "one tm_count per motif" if args.separate else
-                         "one tm_count_multi over the motifs (shared horizons and window-end ranks)"}
+                         "one tm_count_multi over the motifs (shared horizons and window descriptors; a motif "
+                         "that is a prefix of another is counted as that motif's search-tree nodes)",
+                "value_without_prefix_fusion": (roots_per_step * args.steps / (nofuse_ms / 1000)
+                                                if nofuse_ms > 0 else None)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
