@@ -435,7 +435,12 @@ def main():
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": f"mine_kernel<PlanC<{MOTIFS[dom]}>, kCount>",
+                "traffic": traffic,
+                "kernel": f"mine_kernel<PlanC<{MOTIFS[dom]}>, "
+                          + ("kCountPfx> (also counts " + ", ".join(MOTIFS[i] for i in range(len(MOTIFS))
+                                                              if part0['fused_into'][i] == MOTIFS[dom]) + ")"
+                             if any(part0['fused_into'][i] == MOTIFS[dom] for i in range(len(MOTIFS)))
+                             else "kCount>"),
                 "peak_source": peak_src, "per_motif": per_motif,
                 "mine_share_of_step": float(mine_ms.sum() / (total_ms / args.steps))}
     e2e = None
