@@ -297,6 +297,7 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         }
         MineParams p = base;
         p.prefix_mask = pmask[i];
+        p.prefix_lv0 = pmask[i] ? (uint32_t)__builtin_ctz(pmask[i]) : 0u;
         p.L = mo->L;
         for (uint32_t j = 0; j < mo->L; j++) { p.u[j] = mo->u[j]; p.v[j] = mo->v[j]; }
         p.scratch = scratch + (size_t)i * kScratchWords;

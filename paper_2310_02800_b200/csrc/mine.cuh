@@ -70,12 +70,6 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
-// Per-warp shared counters of prefix-fusion matches (lane 0 adds; MineParams::prefix_mask)
-__device__ __forceinline__ unsigned long long *prefix_counters() {
-    __shared__ unsigned long long c[kWarpsPerBlock][kMaxL];
-    return c[threadIdx.x >> 5];
-}
-
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -426,6 +420,7 @@ struct Warp {
     uint64_t cand[LM + 1];
     unsigned long long count;        // lane 0: matches found by batch expansion
     unsigned long long leaf_count;   // per lane: matches found by leaf scans
+    uint32_t pfx_lane;               // per lane: nodes at level prefix_lv0 (kCountPfx)
     Stats st;
 
     __device__ Warp(const MineParams &p_, const Plan &pl, uint32_t *w, int ln) : p(p_), plan(pl), ws(w), lane(ln) {
@@ -433,6 +428,7 @@ struct Warp {
         for (int i = 0; i <= LM; i++) { ntask[i] = 0; cand[i] = 0; }
         count = 0;
         leaf_count = 0;
+        pfx_lane = 0;
         if (MODE == kStats) {
 #pragma unroll
             for (int i = 0; i < kMaxL; i++) st.nodes[i] = 0;
@@ -555,8 +551,12 @@ struct Warp {
                                          const uint32_t (&eh)[NE], uint32_t rslot) {
         uint32_t lo = 0, up = 0;
         if (MODE == kCountPfx && (p.prefix_mask >> NL) & 1u) {   // these nodes are the matches of the NL-edge prefix
-            const uint32_t c = __popc(__ballot_sync(kFull, ok));
-            if (lane == 0) prefix_counters()[NL] += c;
+            if (NL == p.prefix_lv0) {
+                pfx_lane += ok ? 1u : 0u;   // the first masked level: a per-lane counter (no warp op)
+            } else {   // further masked levels (rare: several prefixes of one motif): global atomics
+                const uint32_t c = __popc(__ballot_sync(kFull, ok));
+                if (lane == 0 && c) atomicAdd(p.scratch + kPrefixBase + NL, (unsigned long long)c);
+            }
         }
         if (ok) {
             const uint32_t *hf = p.Hf[NL - 1];
@@ -1120,8 +1120,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (MinBlocks<Plan, MODE>::v
     constexpr int LM = Plan::kL;
     uint32_t *ws = smem + warp * Layout<Plan, MODE>::warp_words();
     const Plan plan(p);
-    if (MODE == kCountPfx && lane < kMaxL) prefix_counters()[lane] = 0;
-    __syncwarp();
     Warp<Plan, MODE> W(p, plan, ws, lane);
     const int L = plan.L();
     uint32_t next = 0, end = 0;
@@ -1214,8 +1212,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (MinBlocks<Plan, MODE>::v
         atomicAdd(p.scratch + kTimeBusy, (unsigned long long)((uint32_t)(te >> 6) - t_start) << 6);
     }
     __syncwarp();
-    if (MODE == kCountPfx && lane < kMaxL && prefix_counters()[lane])
-        atomicAdd(p.scratch + kPrefixBase + lane, prefix_counters()[lane]);
+    if (MODE == kCountPfx) {
+        unsigned long long pl = W.pfx_lane;
+        for (int d = 16; d; d >>= 1) pl += __shfl_xor_sync(kFull, pl, d);
+        if (lane == 0 && pl) atomicAdd(p.scratch + kPrefixBase + p.prefix_lv0, pl);
+    }
     unsigned long long tot = W.leaf_count;
     for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(kFull, tot, d);
     tot += W.count;   // lane 0's batch count (other lanes hold 0)

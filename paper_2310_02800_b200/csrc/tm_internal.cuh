@@ -215,6 +215,7 @@ struct MineParams {
     // created at level l (= the matches of this motif's l-edge prefix) into
     // scratch[kPrefixBase + l]
     uint32_t prefix_mask;
+    uint32_t prefix_lv0;               // lowest set level of prefix_mask (counted per lane)
     // generalized query (PlanR only, gen != 0): labels and anti-edges
     int gen;
     const int32_t *vlab, *elab;        // graph labels (nullptr = all 0)
