@@ -586,3 +586,29 @@ def test_prefix_fusion():
     assert set(carried) == {0, 2, 5, 8}, carried
     assert carried[0] == 1 and carried[2] == 3 and carried[8] == 9
     assert all(kin[i]["grid_ctas"] == 0 for i in carried)
+
+
+def test_prefix_fusion_generic_and_specialised_carriers():
+    """Prefix fusion on the generic kernel (a carrier outside the catalog runs
+    PlanR in the prefix-counting mode), several prefixes of one carrier
+    (PATH2 and P3 inside one 4-edge motif), root ranges, sharing modes, and an
+    NVRTC-specialised carrier (fusion declined, counts unchanged)."""
+    src, dst, t, n = synth.config_graph("C3", m=200_000)
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    d = 86400
+    chord = [(0, 1), (1, 2), (2, 3), (0, 3)]          # not in the catalog
+    specs = [(M.PATH2, d, None), (M.P3, d, None), (chord, d, None)]
+    mos = [T.Motif(mm, dd, ff) for mm, dd, ff in specs]
+    for rr in (None, (50_000, 150_000)):
+        for share in (0, 1, 2):
+            kw = {} if rr is None else {"root_range": rr}
+            got = T.tm_count_multi(g, mos, share=share, **kw)
+            exp = [og.mine(mm, dd, ff, **kw)["count"] for mm, dd, ff in specs]
+            assert got == exp, (rr, share)
+            kin = T.tm_last_kernel_info()
+            assert kin[0]["carried_by"] == 2 and kin[1]["carried_by"] == 2 and kin[2]["carried_by"] == -1
+    spec = T.Motif(chord, d).specialise()
+    got = T.tm_count_multi(g, [T.Motif(M.P3, d), spec])
+    assert got == [og.mine(M.P3, d)["count"], og.mine(chord, d)["count"]]
+    assert [x["carried_by"] for x in T.tm_last_kernel_info()] == [-1, -1]
