@@ -200,15 +200,12 @@ __device__ __forceinline__ void pair_window(const MineParams &p, uint32_t a, uin
     up = first_after32(p.prec, lo, st + len, lim);
 }
 
+// saturating arithmetic of the per-level candidate hints (Warp::cand)
+__device__ __forceinline__ uint32_t cand_add(uint32_t c, uint32_t a) { return c > 0x7FFFFFFFu - a ? 0x7FFFFFFFu : c + a; }
+__device__ __forceinline__ uint32_t cand_sub(uint32_t c, uint32_t a) { return c > a ? c - a : 0u; }
+
 __device__ __forceinline__ uint32_t ceil_log2p1(uint32_t len) {  // ceil(log2(len+1))
     return len ? 32 - __clz(len) : 0;
-}
-
-// Exact warp sum of values < 2^31 as u64.
-__device__ __forceinline__ uint64_t warp_sum_u31(uint32_t v) {
-    uint32_t lo = __reduce_add_sync(kFull, v & 0xffffu);
-    uint32_t hi = __reduce_add_sync(kFull, v >> 16);
-    return ((uint64_t)hi << 16) + lo;
 }
 
 // ------------------------------------------------------------------ plans
@@ -417,7 +414,11 @@ struct Warp {
     uint32_t *ws;
     int lane;
     uint32_t ntask[LM + 1];
-    uint64_t cand[LM + 1];
+    // candidates pending per level (Σ window sizes of its tasks): a scheduling
+    // hint only (correctness never depends on it) kept in u32 — window sizes
+    // are clamped to 2^26 when added and subtractions saturate at 0, so it
+    // never exceeds the true value and is exact below 2^26 per window
+    uint32_t cand[LM + 1];
     unsigned long long count;        // lane 0: matches found by batch expansion
     unsigned long long leaf_count;   // per lane: matches found by leaf scans
     uint32_t pfx_lane;               // per lane: nodes at level prefix_lv0 (kCountPfx)
@@ -759,7 +760,7 @@ struct Warp {
             if constexpr (MODE == kRoots) fld<NL, Lay::rs(NL)>()[slot] = rslot;
         }
         ntask[NL] += __popc(mask);
-        cand[NL] += warp_sum_u31(keep ? up - lo : 0u);
+        cand[NL] = cand_add(cand[NL], __reduce_add_sync(kFull, keep ? min(up - lo, 1u << 26) : 0u));
         __syncwarp();
     }
 
@@ -869,7 +870,7 @@ struct Warp {
         // consume: pop the fully taken tasks, advance the partially taken one
         if (takes && !full) flo[j] = lo + (32u - excl);
         ntask[LV] = n - kfull;
-        cand[LV] -= C;
+        cand[LV] = cand_sub(cand[LV], C);
         __syncwarp();
 
         if (LV + 1 == plan.L()) {
@@ -937,12 +938,12 @@ struct Warp {
         __syncwarp();
         if (split) {
             if (lane == 0) base[kCap + j] = mid;          // kept: [lo, mid)
-            cand[LV] -= up - mid;
+            cand[LV] = cand_sub(cand[LV], up - mid);
         } else {                                          // the top task fills slot j
             const uint32_t top = ntask[LV] - 1;
             if (lane < F) base[lane * kCap + j] = base[lane * kCap + top];
             ntask[LV] = top;
-            cand[LV] -= up - lo;
+            cand[LV] = cand_sub(cand[LV], up - lo);
         }
         __syncwarp();
     }
@@ -956,7 +957,7 @@ struct Warp {
         if (lane < F) base[lane * kCap + slot] = val;
         const uint32_t lo = __shfl_sync(kFull, val, 0), up = __shfl_sync(kFull, val, 1);
         ntask[LV] = slot + 1;
-        cand[LV] += up - lo;
+        cand[LV] = cand_add(cand[LV], min(up - lo, 1u << 26));
         __syncwarp();
     }
 
