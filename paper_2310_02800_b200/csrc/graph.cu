@@ -54,8 +54,11 @@ __global__ void k_bias(uint32_t *off, uint32_t n1, uint32_t bias) {
 // block stages T over that range in shared memory (coalesced) and every
 // thread binary-searches there.  Bursty stretches whose range exceeds the
 // stage fall back to a per-thread gallop in global memory.
-constexpr int kHB = 512;       // edges per block
-constexpr int kHStage = 3072;  // staged timestamps (24 KB)
+#ifndef TM_HB
+#define TM_HB 512
+#endif
+constexpr int kHB = TM_HB;          // edges per block
+constexpr int kHStage = 6 * kHB;    // staged timestamps (24 KB at 512)
 
 __device__ __forceinline__ uint64_t horizon_one(const int64_t *__restrict__ T, uint64_t m, int64_t d, uint64_t e) {
     const int64_t te = T[e];
