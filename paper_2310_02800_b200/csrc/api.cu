@@ -73,17 +73,22 @@ bool is_specialised(uint64_t code) {
 }
 
 KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised, bool generic) {
-    if (!generic && (mode == kCount || mode == kEnum || mode == kCountPfx)) {
-        for (auto &e : catalog())
-            if (e.code == code && (mode != kCountPfx || e.count_pfx.fn)) {
-                if (specialised) *specialised = true;
-                return mode == kCount ? e.count : mode == kEnum ? e.enumerate : e.count_pfx;
-            }
+    if (!generic && (mode == kCount || mode == kEnum || mode == kCountPfx || mode == kResume || mode == kCountSib)) {
+        for (auto &e : catalog()) {
+            if (e.code != code) continue;
+            const KernelInfo &ki = mode == kCount ? e.count : mode == kEnum ? e.enumerate
+                                 : mode == kCountPfx ? e.count_pfx : mode == kResume ? e.resume : e.count_sib;
+            if (!ki.fn) break;
+            if (specialised) *specialised = true;
+            return ki;
+        }
     }
     if (specialised) *specialised = false;
     switch (mode) {
         case kCount: return kernel_info<PlanR, kCount>();
         case kCountPfx: return kernel_info<PlanR, kCountPfx>();
+        case kResume: return kernel_info<PlanR, kResume>();
+        case kCountSib: return kernel_info<PlanR, kCountSib>();
         case kEnum: return kernel_info<PlanR, kEnum>();
         case kRoots: return kernel_info<PlanR, kRoots>();
         default: return kernel_info<PlanR, kStats>();
@@ -187,6 +192,77 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         }
     }
 
+    // sibling emission + resume: motif B = A's first K edges + one closing edge
+    // whose candidates are A's level-K candidates (same list, same window), A
+    // continuing past level K+1: A's kernel writes B's matches as rows; B's
+    // count is their number, and a motif D that starts with B continues from
+    // those rows at level K+1 (a kResume kernel) instead of searching again
+    std::vector<int> sib_of(k, -1), resume_of(k, -1);
+    std::vector<uint32_t> sib_vtx(k, 0), sib_K(k, 0);
+    if (mode == kCount && o.fuse == 0 && k > 1) {
+        auto eff = [](const tm_motif *mo, uint32_t g) {
+            const int64_t f = mo->fine[g];
+            return (f == TM_DELTA_INF || f >= mo->delta) ? TM_DELTA_INF : f;
+        };
+        auto shape = [](const tm_motif *mo) {
+            Shape sh{};
+            sh.L = (int)mo->L;
+            for (uint32_t j = 0; j < mo->L; j++) { sh.u[j] = mo->u[j]; sh.v[j] = mo->v[j]; }
+            return sh;
+        };
+        auto plain = [](const tm_motif *mo) { return !mo->constrained() && !mo->rtc_fn[kCount]; };
+        for (uint32_t b = 0; b < k; b++) {   // B: a sibling of a launched motif A
+            const tm_motif *mb = mos[b];
+            if (!plain(mb) || mb->L < 2) continue;
+            const uint32_t K = mb->L - 1;
+            if (K != (uint32_t)kSibLevel) continue;   // the kCountSib kernels emit at level 2
+            const Shape sb = shape(mb);
+            const int nbk = sb.nv((int)K);
+            if (!(sb.u[K] < nbk && sb.v[K] < nbk)) continue;   // B's last edge must close (both ends mapped)
+            for (uint32_t a = 0; a < k && sib_of[b] < 0; a++) {
+                const tm_motif *ma = mos[a];
+                if (a == b || sib_of[a] >= 0 || !plain(ma) || ma->L < K + 2 ||
+                    ma->delta != mb->delta)
+                    continue;
+                if (motif_code((int)K, ma->u, ma->v) != motif_code((int)K, mb->u, mb->v)) continue;
+                bool same = true;
+                for (uint32_t g = 0; g < K; g++) same &= eff(ma, g) == eff(mb, g);
+                if (!same) continue;
+                const Shape sa = shape(ma);
+                const int nak = sa.nv((int)K);
+                if (sa.u[K] < nak && sa.v[K] < nak) continue;        // A's edge K must be open (full windows)
+                if (sa.ldir((int)K) != sb.ldir((int)K) || sa.lx((int)K) != sb.lx((int)K)) continue;
+                sib_of[b] = (int)a;
+                sib_K[b] = K;
+                sib_vtx[b] = (uint32_t)(sb.ldir((int)K) == 0 ? sb.v[K] : sb.u[K]);
+            }
+        }
+        for (uint32_t d = 0; d < k; d++) {   // D: continues from the rows of a sibling B
+            const tm_motif *md = mos[d];
+            if (sib_of[d] >= 0 || !plain(md)) continue;
+            for (uint32_t b = 0; b < k && resume_of[d] < 0; b++) {
+                const tm_motif *mb = mos[b];
+                if (sib_of[b] < 0 || (int)d == sib_of[b] || md->L <= mb->L || md->delta != mb->delta) continue;
+                if (motif_code((int)mb->L, md->u, md->v) != mb->code) continue;
+                bool same = true;
+                for (uint32_t g = 0; g + 1 < mb->L; g++) same &= eff(md, g) == eff(mb, g);
+                if (same) resume_of[d] = (int)b;
+            }
+        }
+    }
+    // at most one sibling per carrier kernel
+    {
+        std::vector<int> taken(k, 0);
+        for (uint32_t b = 0; b < k; b++)
+            if (sib_of[b] >= 0) {
+                if (taken[sib_of[b]]) sib_of[b] = -1;
+                else taken[sib_of[b]] = 1;
+            }
+        for (uint32_t d = 0; d < k; d++)
+            if (resume_of[d] >= 0 && sib_of[resume_of[d]] < 0) resume_of[d] = -1;
+    }
+    // a carrier of a sibling runs in the kCountPfx mode; prefix fusion of the
+    // sibling's own prefixes is unaffected
     // prefix fusion (counting): the longest motifs run their kernels; a motif
     // that is the first l edges of one of them, with the same δ and effective
     // δ_1..δ_{l-1} and no constraints, is counted there as its level-l nodes
@@ -203,11 +279,12 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         for (uint32_t a = 0; a < k; a++) {
             const uint32_t i = order[a];
             const tm_motif *mi = mos[i];
-            if (mi->constrained()) continue;
+            if (mi->constrained() || sib_of[i] >= 0 || resume_of[i] >= 0) continue;
             for (uint32_t b = 0; b < a && carrier[i] < 0; b++) {
                 const uint32_t j = order[b];
                 const tm_motif *mj = mos[j];
-                if (carrier[j] >= 0 || mj->constrained() || mj->rtc_fn[kCount] || mj->L <= mi->L ||
+                if (carrier[j] >= 0 || sib_of[j] >= 0 || resume_of[j] >= 0 || mj->constrained() ||
+                    mj->rtc_fn[kCount] || mj->L <= mi->L ||
                     mj->delta != mi->delta)
                     continue;
                 if (motif_code((int)mi->L, mj->u, mj->v) != mi->code) continue;
@@ -219,6 +296,9 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             }
         }
     }
+
+    uint32_t *sib_rows = nullptr;
+    uint64_t sib_cap = 0;
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evd = nullptr;
     std::vector<cudaEvent_t> evk(k, nullptr);
@@ -289,15 +369,60 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
     cudaGetDevice(&dev);
     TM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int threads = kWarpsPerBlock * 32;
-    for (uint32_t i = 0; i < k; i++) {
+    // sibling rows: one region per sibling motif (cap rows of L_b edge ids)
+    std::vector<uint32_t *> sib_region(k, nullptr);
+    {
+        uint64_t words = 0;
+        sib_cap = std::min<uint64_t>(std::max<uint64_t>(base.n_roots, 1u << 16), 1u << 22);
+        for (uint32_t b = 0; b < k; b++)
+            if (sib_of[b] >= 0) words += sib_cap * mos[b]->L;
+        if (words) {
+            TM_CUDA_TRY(dev_alloc((void **)&sib_rows, words * sizeof(uint32_t), s));
+            fr.v.push_back(sib_rows);
+            uint64_t off = 0;
+            for (uint32_t b = 0; b < k; b++)
+                if (sib_of[b] >= 0) {
+                    sib_region[b] = sib_rows + off;
+                    off += sib_cap * mos[b]->L;
+                }
+        }
+    }
+    // launch order: every searching kernel, then the kernels resuming from sibling rows
+    std::vector<uint32_t> ord;
+    for (uint32_t i = 0; i < k; i++)
+        if (resume_of[i] < 0) ord.push_back(i);
+    for (uint32_t i = 0; i < k; i++)
+        if (resume_of[i] >= 0) ord.push_back(i);
+    std::vector<int> pos_of(k, 0);
+    for (uint32_t oi = 0; oi < k; oi++) pos_of[ord[oi]] = (int)oi;
+    for (uint32_t oi = 0; oi < k; oi++) {
+        const uint32_t i = ord[oi];
         const tm_motif *mo = mos[i];
-        if (carrier[i] >= 0) {   // counted inside its carrier's kernel
+        if (carrier[i] >= 0 || sib_of[i] >= 0) {   // counted inside another motif's kernel
             TM_CUDA_TRY(cudaEventRecord(evk[i], s));
             continue;
         }
         MineParams p = base;
         p.prefix_mask = pmask[i];
         p.prefix_lv0 = pmask[i] ? (uint32_t)__builtin_ctz(pmask[i]) : 0u;
+        for (uint32_t b = 0; b < k; b++)
+            if (sib_of[b] == (int)i) {   // this kernel emits sibling b's matches as rows
+                p.sib_level = sib_K[b];
+                p.sib_vtx = sib_vtx[b];
+                p.sib_rows = sib_region[b];
+                p.sib_cap = (uint32_t)sib_cap;
+            }
+        const bool resuming = resume_of[i] >= 0;
+        if (resuming) {   // continue from sibling b's rows
+            const int b = resume_of[i];
+            p.resume_rows = sib_region[b];
+            p.resume_n = scratch + (size_t)sib_of[b] * kScratchWords + kSibCount;
+            p.resume_level = mos[b]->L;
+            p.sib_cap = (uint32_t)sib_cap;
+            p.roots = nullptr;
+            p.root_lo = 0;
+            p.n_roots = sib_cap;   // grid sizing; the kernel reads the row count
+        }
         p.L = mo->L;
         for (uint32_t j = 0; j < mo->L; j++) { p.u[j] = mo->u[j]; p.v[j] = mo->v[j]; }
         p.scratch = scratch + (size_t)i * kScratchWords;
@@ -330,7 +455,9 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             bool spec = false;
             // a runtime-specialised kernel (tm_motif_specialise) first, then the
             // build-time catalog, then the generic kernel
-            const int kmode = (mode == kCount && p.prefix_mask) ? (int)kCountPfx : mode;
+            const int kmode = resuming ? (int)kResume
+                              : (mode == kCount && p.sib_level) ? (int)kCountSib
+                              : (mode == kCount && p.prefix_mask) ? (int)kCountPfx : mode;
             void *rfn = (kmode == kCount || kmode == kEnum) ? mo->rtc_fn[kmode] : nullptr;
             KernelInfo ki{nullptr, 0};
             if (!rfn) ki = lookup_kernel(mo->code, kmode, &spec, mo->constrained());
@@ -407,12 +534,12 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
     TM_CUDA_TRY(cudaEventRecord(evd, s));
     TM_CUDA_TRY(cudaStreamSynchronize(s));
     cudaEventElapsedTime(&g_info.horizon_ms, ev0, ev1);
-    cudaEventElapsedTime(&g_info.mine_ms, ev1, evk[k - 1]);
+    cudaEventElapsedTime(&g_info.mine_ms, ev1, evk[ord.back()]);
     cudaEventElapsedTime(&g_info.total_ms, ev0, evd);
     for (uint32_t i = 0; i < k; i++) {
         const unsigned long long *h = host.data() + (size_t)i * kScratchWords;
         tm_kernel_info &ki = g_kinfo[i];
-        cudaEventElapsedTime(&ki.mine_ms, i ? evk[i - 1] : ev1, evk[i]);
+        cudaEventElapsedTime(&ki.mine_ms, pos_of[i] ? evk[ord[pos_of[i] - 1]] : ev1, evk[i]);
         ki.shared_tasks = h[kShareDone];
         if (h[kTimeStart] && h[kTimeExit]) {
             const unsigned long long t0 = ~h[kTimeStart], te = h[kTimeExit];
@@ -428,6 +555,10 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             out[i].count = host[(size_t)carrier[i] * kScratchWords + kPrefixBase + mos[i]->L];
             ki = tm_kernel_info{};
             ki.carried_by = carrier[i];
+        } else if (sib_of[i] >= 0) {   // sibling: the number of rows its carrier emitted
+            out[i].count = host[(size_t)sib_of[i] * kScratchWords + kSibCount];
+            ki = tm_kernel_info{};
+            ki.carried_by = sib_of[i];
         }
         for (int w = 0; w < kScratchWords; w++) out[i].stats[w] = h[w];
 #ifdef TM_PHASE_PROFILE
@@ -438,6 +569,23 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
                         (double)h[20 + 2 * l] / h[21 + 2 * l], 0.0 + h[20 + 2 * l]);
         fprintf(stderr, "\n");
 #endif
+    }
+    // a sibling with more matches than row slots: its resuming motifs are
+    // counted again from scratch (without fusion)
+    for (uint32_t d = 0; d < k; d++) {
+        if (resume_of[d] < 0) continue;
+        const int b = resume_of[d];
+        if (host[(size_t)sib_of[b] * kScratchWords + kSibCount] <= sib_cap) continue;
+        const std::vector<tm_kernel_info> keep = g_kinfo;
+        const tm_run_info keep_info = g_info;
+        tm_run_opts o2 = o;
+        o2.fuse = 1;
+        RunOut r2;
+        const tm_status st = run_multi(g, &mos[d], 1, &o2, mode, nullptr, 0, nullptr, 0, nullptr, &r2);
+        g_kinfo = keep;
+        g_info = keep_info;
+        if (st) return st;
+        out[d].count = r2.count;
     }
     // the last motif's load balance in the single-query record
     g_info.shared_tasks = g_kinfo[k - 1].shared_tasks;

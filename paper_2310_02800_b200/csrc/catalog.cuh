@@ -20,14 +20,20 @@ constexpr uint64_t mcode(int L, int a0, int b0, int a1 = 0, int b1 = 0, int a2 =
 struct CatalogEntry {
     uint64_t code;
     KernelInfo count, enumerate;
-    KernelInfo count_pfx;   // counting + prefix fusion (named motifs); fn == nullptr: not instantiated
+    KernelInfo count_pfx;   // counting + prefix fusion / sibling emission (named motifs); fn == nullptr: none
+    KernelInfo resume;      // counting resumed from rows of partial matches (named motifs)
+    KernelInfo count_sib;   // kCountPfx + sibling rows at level 2 (named motifs of >= 4 edges)
 };
 
 template <uint64_t CODE, bool PFX = false>
 CatalogEntry entry() {
-    KernelInfo pfx{nullptr, 0};
-    if constexpr (PFX) pfx = kernel_info<PlanC<CODE>, kCountPfx>();
-    return CatalogEntry{CODE, kernel_info<PlanC<CODE>, kCount>(), kernel_info<PlanC<CODE>, kEnum>(), pfx};
+    KernelInfo pfx{nullptr, 0}, res{nullptr, 0}, sib{nullptr, 0};
+    if constexpr (PFX) {
+        pfx = kernel_info<PlanC<CODE>, kCountPfx>();
+        res = kernel_info<PlanC<CODE>, kResume>();
+        if constexpr (PlanC<CODE>::kL >= 4) sib = kernel_info<PlanC<CODE>, kCountSib>();
+    }
+    return CatalogEntry{CODE, kernel_info<PlanC<CODE>, kCount>(), kernel_info<PlanC<CODE>, kEnum>(), pfx, res, sib};
 }
 
 void register_named(std::vector<CatalogEntry> &v);

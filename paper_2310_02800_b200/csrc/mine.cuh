@@ -366,9 +366,13 @@ struct PlanR {
 template <class Plan, int MODE>
 struct Layout {
     // [0] lo  [1] up  [2 ..) kept φ slots  [hi]  kept matched edge ids  [root slot (kRoots)]
-    __host__ __device__ static constexpr bool kphi(int l, int k) { return MODE == kStats || Plan::keep_phi(l, k); }
+    // kCountSib keeps every φ slot and matched id up to its sibling level: the rows read them
+    __host__ __device__ static constexpr bool kphi(int l, int k) {
+        return MODE == kStats || (MODE == kCountSib && l <= kSibLevel) || Plan::keep_phi(l, k);
+    }
     __host__ __device__ static constexpr bool keh(int l, int k) {
-        return k < l && (MODE == kEnum || MODE == kStats || Plan::keep_eh(l, k));
+        return k < l && (MODE == kEnum || MODE == kStats || (MODE == kCountSib && l <= kSibLevel) ||
+                         Plan::keep_eh(l, k));
     }
     __host__ __device__ static constexpr bool khi(int l) { return MODE == kStats || Plan::keep_hi(l); }
     __host__ __device__ static constexpr int phi(int l, int k) {
@@ -422,6 +426,7 @@ struct Warp {
     unsigned long long count;        // lane 0: matches found by batch expansion
     unsigned long long leaf_count;   // per lane: matches found by leaf scans
     uint32_t pfx_lane;               // per lane: nodes at level prefix_lv0 (kCountPfx)
+    uint32_t n_items;                // roots (or, kResume, rows) this launch mines
     Stats st;
 
     __device__ Warp(const MineParams &p_, const Plan &pl, uint32_t *w, int ln) : p(p_), plan(pl), ws(w), lane(ln) {
@@ -430,6 +435,18 @@ struct Warp {
         count = 0;
         leaf_count = 0;
         pfx_lane = 0;
+        n_items = (uint32_t)p.n_roots;
+        if (MODE == kResume) {
+            unsigned long long n = 0;
+            if (ln == 0) n = *reinterpret_cast<const volatile unsigned long long *>(p.resume_n);
+            n = __shfl_sync(kFull, n, 0);
+            n_items = (uint32_t)min(n, (unsigned long long)p.sib_cap);
+#ifdef TM_DEBUG_RESUME
+            if (ln == 0 && blockIdx.x == 0 && threadIdx.x == 0)
+                printf("[resume] n=%llu cap=%u level=%u rows=%p row0=%u %u %u\n", n, p.sib_cap, p.resume_level,
+                       (const void *)p.resume_rows, p.resume_rows[0], p.resume_rows[1], p.resume_rows[2]);
+#endif
+        }
         if (MODE == kStats) {
 #pragma unroll
             for (int i = 0; i < kMaxL; i++) st.nodes[i] = 0;
@@ -551,7 +568,7 @@ struct Warp {
     __device__ __forceinline__ void push(bool ok, uint32_t e, uint32_t hi, const uint32_t (&phi)[NS],
                                          const uint32_t (&eh)[NE], uint32_t rslot) {
         uint32_t lo = 0, up = 0;
-        if (MODE == kCountPfx && (p.prefix_mask >> NL) & 1u) {   // these nodes are the matches of the NL-edge prefix
+        if ((MODE == kCountPfx || MODE == kCountSib) && (p.prefix_mask >> NL) & 1u) {   // matches of the NL-edge prefix
             if (NL == p.prefix_lv0) {
                 pfx_lane += ok ? 1u : 0u;   // the first masked level: a per-lane counter (no warp op)
             } else {   // further masked levels (rare: several prefixes of one motif): global atomics
@@ -766,19 +783,60 @@ struct Warp {
 
     // Take up to 32 roots from the global cursor and bind motif edge 1 to them
     // (the root level maps motif edge 1 onto every graph edge).
+    // kResume: row `slot` holds the NL edge ids of a partial match of this
+    // motif's first NL edges (emitted by another kernel, sibling emission):
+    // rebuild φ and continue the search at level NL exactly as if this kernel
+    // had created that node itself
+    template <int NL>
+    __device__ __forceinline__ void resume(bool ok, uint32_t slot) {
+        constexpr int S = Plan::nslots(NL);
+        uint32_t eh[NL], phi[S + 1];
+#pragma unroll
+        for (int k = 0; k < S + 1; k++) phi[k] = 0u;
+        uint32_t hi = 0;
+        if (ok) {
+            const uint32_t *row = p.resume_rows + (size_t)slot * NL;
+            sfor<NL>([&](auto ic_) {
+                constexpr int i = decltype(ic_)::value;
+                eh[i] = __ldg(row + i);
+                const uint32_t a = __ldg(p.src + eh[i]), b = __ldg(p.dst + eh[i]);
+#pragma unroll
+                for (int k = 0; k < S; k++) {
+                    if (k == plan.template u<i>()) phi[k] = a;
+                    if (k == plan.template v<i>()) phi[k] = b;
+                }
+            });
+            hi = __ldg(p.H + eh[0]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < NL; i++) eh[i] = 0u;
+        }
+        push<NL>(ok, eh[NL - 1], hi, phi, eh, slot);
+    }
+
     // next/end: this warp's claimed root slots (u32: n_roots <= m < 2^31)
     __device__ __forceinline__ bool fetch_roots(uint32_t &next, uint32_t &end) {
         if (next >= end) {
             unsigned long long b = 0;
             if (lane == 0) b = atomicAdd(&p.scratch[0], (unsigned long long)kRootChunk);
             b = __shfl_sync(kFull, b, 0);
-            if (b >= p.n_roots) return false;
+            if (b >= n_items) return false;
             next = (uint32_t)b;
-            end = (uint32_t)min((uint64_t)(b + kRootChunk), (uint64_t)p.n_roots);
+            end = (uint32_t)min((uint64_t)(b + kRootChunk), (uint64_t)n_items);
         }
         const uint32_t slot = next + lane;
         bool ok = slot < end;
         next = min(next + 32u, end);
+        if constexpr (MODE == kResume) {   // rows of partial matches: continue at level resume_level
+            switch (p.resume_level) {
+                case 2: if constexpr (LM > 2) resume<2>(ok, slot); break;
+                case 3: if constexpr (LM > 3) resume<3>(ok, slot); break;
+                case 4: if constexpr (LM > 4) resume<4>(ok, slot); break;
+                case 5: if constexpr (LM > 5) resume<5>(ok, slot); break;
+                default: break;
+            }
+            return true;
+        }
         uint32_t r = 0, a = 0, bb = 0;
         if (ok) {
             r = (uint32_t)(p.roots ? p.roots[slot] : p.root_lo + slot);
@@ -863,6 +921,26 @@ struct Warp {
                 if (gen() && ok) {
                     const int nb = plan.template nv<LV>();
                     ok = labels_ok(LV, e, nb < plan.template nv<LV + 1>(), nb, w);
+                }
+            }
+        }
+        if constexpr (MODE == kCountSib && LV == kSibLevel) {
+            {   // sibling emission: a closing edge to φ[sib_vtx] on this candidate
+                const bool sib = active && w == pick(phi, p.sib_vtx);
+                const uint32_t smask = __ballot_sync(kFull, sib);
+                if (smask) {
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(p.scratch + kSibCount, (unsigned long long)__popc(smask));
+                    base = __shfl_sync(kFull, base, 0);
+                    if (sib) {
+                        const unsigned long long row = base + __popc(smask & lanemask_lt());
+                        if (row < p.sib_cap) {
+                            uint32_t *dst = p.sib_rows + row * (LV + 1);
+#pragma unroll
+                            for (int i = 0; i < LV; i++) dst[i] = eh[i];
+                            dst[LV] = e;
+                        }
+                    }
                 }
             }
         }
@@ -1106,6 +1184,10 @@ struct MinBlocks<PlanC<CODE, false>, kCount> {
 };
 template <uint64_t CODE>
 struct MinBlocks<PlanC<CODE, false>, kCountPfx> : MinBlocks<PlanC<CODE, false>, kCount> {};
+template <uint64_t CODE>
+struct MinBlocks<PlanC<CODE, false>, kResume> : MinBlocks<PlanC<CODE, false>, kCount> {};
+template <uint64_t CODE>
+struct MinBlocks<PlanC<CODE, false>, kCountSib> : MinBlocks<PlanC<CODE, false>, kCount> {};
 #ifndef TM_MIN_BLOCKS_ENUM
 #define TM_MIN_BLOCKS_ENUM 4
 #endif
@@ -1213,7 +1295,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (MinBlocks<Plan, MODE>::v
         atomicAdd(p.scratch + kTimeBusy, (unsigned long long)((uint32_t)(te >> 6) - t_start) << 6);
     }
     __syncwarp();
-    if (MODE == kCountPfx) {
+    if (MODE == kCountPfx || MODE == kCountSib) {
         unsigned long long pl = W.pfx_lane;
         for (int d = 16; d; d >>= 1) pl += __shfl_xor_sync(kFull, pl, d);
         if (lane == 0 && pl) atomicAdd(p.scratch + kPrefixBase + p.prefix_lv0, pl);

@@ -166,7 +166,12 @@ namespace tmg {
 // kCountPfx: counting that also counts the nodes of the levels in
 // MineParams::prefix_mask (prefix fusion, tm_count_multi) — a separate
 // instantiation, so the plain counting kernels carry none of that code.
-enum Mode : int { kCount = 0, kEnum = 1, kRoots = 2, kStats = 3, kCountPfx = 4 };
+// kResume: counting that starts from rows of partial matches (sibling
+// emission of another kernel) instead of root edges.
+// kCountSib: kCountPfx plus sibling emission at level 2 (level-2 tasks keep
+// every φ slot and matched id for the rows).
+enum Mode : int { kCount = 0, kEnum = 1, kRoots = 2, kStats = 3, kCountPfx = 4, kResume = 5, kCountSib = 6 };
+constexpr int kSibLevel = 2;   // the level kCountSib kernels emit sibling rows at
 
 // Packed motif structure: bits 0-2 L, then per edge i: u at 3+6i, v at 6+6i.
 constexpr uint64_t motif_code(int L, const uint8_t *u, const uint8_t *v) {
@@ -216,6 +221,16 @@ struct MineParams {
     // scratch[kPrefixBase + l]
     uint32_t prefix_mask;
     uint32_t prefix_lv0;               // lowest set level of prefix_mask (counted per lane)
+    // sibling emission (kCountPfx): at level sib_level, candidates whose
+    // neighbour is φ[sib_vtx] complete a sibling motif's closing edge; their
+    // rows (e_1..e_sib_level, e) go to sib_rows (cap rows), counted in
+    // scratch[kSibCount]
+    uint32_t sib_level, sib_vtx, sib_cap;
+    uint32_t *sib_rows;
+    // resume (kResume): rows of resume_level edge ids, *resume_n of them (<= sib_cap)
+    const uint32_t *resume_rows;
+    const unsigned long long *resume_n;
+    uint32_t resume_level;
     // generalized query (PlanR only, gen != 0): labels and anti-edges
     int gen;
     const int32_t *vlab, *elab;        // graph labels (nullptr = all 0)
@@ -238,6 +253,7 @@ constexpr int kTimeStart = 40, kTimeDrain = 41, kTimeExit = 42, kTimeBusy = 43, 
 // warps (an int in the low half), subtrees handed over
 constexpr int kShareTail = 3, kShareHead = 4, kShareIdle = 5, kShareDone = 6;
 constexpr int kShareWords = 32;   // u32 words per shared task record (fields + level in word 31)
+constexpr int kSibCount = 45;     // scratch[45]: sibling rows emitted (all, even beyond sib_cap)
 constexpr int kPrefixBase = 32;   // scratch[32 + l]: prefix matches (nodes created at level l)
 constexpr int kStatsBase = 8;   // scratch[8 + l] nodes[l], [16] window, [17] list, [18] probes, [19] fast window
 
