@@ -302,6 +302,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     balance = [None] * len(MOTIFS)   # load balance of the last step's mining kernels (§8 a8)
     fused_into = [None] * len(MOTIFS)   # prefix fusion: the motif whose kernel counted this one
+    kernel_mode = [0] * len(MOTIFS)     # tm_kernel_info.kernel_mode of the last step
 
     def step(g, rr):
         if args.separate:   # one tm_count per motif, each building its own horizons
@@ -320,6 +321,7 @@ def main():
         for i, x in enumerate(kin):
             balance[i] = {"shared_tasks": x["shared_tasks"], "tail_ms": x["tail_ms"], "warp_busy": x["warp_busy"]}
             fused_into[i] = MOTIFS[x["carried_by"]] if x["carried_by"] >= 0 else None
+            kernel_mode[i] = x["kernel_mode"]
         return cs, [x["mine_ms"] for x in kin], T.tm_last_run_info()["launches"]
 
     def timed(fn):
@@ -371,6 +373,7 @@ def main():
                 part0["mine_ms"] = mm0
                 part0["balance"] = [dict(x) for x in balance]
                 part0["fused_into"] = list(fused_into)
+                part0["kernel_mode"] = list(kernel_mode)
             g.close()
             del g
             # ---- end to end through the public API from pinned host memory
@@ -418,13 +421,20 @@ def main():
         bytes_q.append(bq)
         ms = part0["mine_ms"][i]
         fz = part0["fused_into"][i]
+        resumed = part0.get("kernel_mode", [0] * len(MOTIFS))[i] == 5   # kResume: not a full search
         per_motif.append({"motif": name, "count": counts[i], "mine_ms": None if fz else ms,
-                          "alg_bytes": bq, "alg_GBps": None if fz else bq / (ms / 1000) / 1e9,
+                          "alg_bytes": bq, "alg_GBps": None if fz or resumed else bq / (ms / 1000) / 1e9,
+                          "resumed_from_rows": resumed,
                           "search_nodes": sum(part0["stats"][i]["nodes"][1:L]),
                           "window_sum": part0["stats"][i]["window_sum"],
                           "load_balance": None if fz else part0["balance"][i],
                           "counted_inside": fz})
     dom = int(np.argmax(part0["mine_ms"]))
+
+    def kernel_label(d, kmode, fused):
+        name = {0: "kCount", 1: "kEnum", 4: "kCountPfx", 5: "kResume", 6: "kCountSib"}.get(kmode, str(kmode))
+        inside = [MOTIFS[i] for i in range(len(MOTIFS)) if fused[i] == MOTIFS[d]]
+        return f"mine_kernel<PlanC<{MOTIFS[d]}>, {name}>" + (f" (also counts {', '.join(inside)})" if inside else "")
     peak, peak_src = peaks()
     achieved = bytes_q[dom] / (part0["mine_ms"][dom] / 1000) / 1e9
     traffic = None
@@ -436,11 +446,7 @@ def main():
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic,
-                "kernel": f"mine_kernel<PlanC<{MOTIFS[dom]}>, "
-                          + ("kCountPfx> (also counts " + ", ".join(MOTIFS[i] for i in range(len(MOTIFS))
-                                                              if part0['fused_into'][i] == MOTIFS[dom]) + ")"
-                             if any(part0['fused_into'][i] == MOTIFS[dom] for i in range(len(MOTIFS)))
-                             else "kCount>"),
+                "kernel": kernel_label(dom, part0.get("kernel_mode", [0] * len(MOTIFS))[dom], part0["fused_into"]),
                 "peak_source": peak_src, "per_motif": per_motif,
                 "mine_share_of_step": float(mine_ms.sum() / (total_ms / args.steps))}
     e2e = None

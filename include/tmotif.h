@@ -233,9 +233,16 @@ tm_status tm_search_stats_run(const tm_graph *g, const tm_motif *mo, const tm_ru
  * tm_count of mos[i].  The query-time structures — the δ-horizons of every
  * distinct δ / δ_i and the window-end ranks of every
  * distinct (list, gap bound) — are built once and shared, then one mining
- * kernel per motif runs on o->stream.  mos: k host pointers; counts: host,
- * k entries.  Synchronous.  Errors: as tm_count; TM_EINVAL for k == 0.
- * tm_last_kernel_info reports each motif's kernel. */
+ * kernel per motif runs on o->stream.  Unless o->fuse == 1, a motif that is
+ * the first l edges of another (same δ, δ_i, no constraints) is counted as
+ * that motif's level-l search nodes (Alg. 1 creates one per prefix match); a
+ * motif that differs from another only in its last edge's target (a
+ * "sibling", e.g. TRI of the 4-cycle) is written as rows (its matches) by
+ * that motif's kernel, and a motif extending the sibling resumes its search
+ * from those rows (a row buffer overflow re-counts it without fusion).  The
+ * counts are the same with or without fusion.  mos: k host pointers;
+ * counts: host, k entries.  Synchronous.  Errors: as tm_count; TM_EINVAL
+ * for k == 0.  tm_last_kernel_info reports each motif's kernel. */
 tm_status tm_count_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, const tm_run_opts *o,
                          uint64_t *counts);
 
@@ -248,8 +255,17 @@ typedef struct {
     float warp_busy;
     uint32_t grid_ctas;
     uint64_t shared_tasks;
-    int32_t carried_by;      /* prefix fusion: index of the motif whose kernel counted this one, else -1 */
+    int32_t carried_by;      /* fusion: index of the motif whose kernel counted this one (as a prefix or
+                                as sibling rows), else -1 */
+    int32_t kernel_mode;     /* which kernel ran: TM_KMODE_* below; TM_KMODE_NONE when carried */
 } tm_kernel_info;
+
+#define TM_KMODE_NONE (-1)      /* no kernel of its own (carried_by >= 0, or no roots) */
+#define TM_KMODE_COUNT 0        /* plain count (Alg. 1) */
+#define TM_KMODE_ENUM 1         /* enumeration */
+#define TM_KMODE_COUNT_PREFIX 4 /* count that also counts carried prefix motifs */
+#define TM_KMODE_RESUME 5       /* count resumed from the sibling rows of another kernel */
+#define TM_KMODE_COUNT_SIB 6    /* count that also writes a carried sibling motif's matches as rows */
 
 /* Copies min(cap, n) entries to out (host); *n = number of kernels. */
 tm_status tm_last_kernel_info(tm_kernel_info *out, uint32_t cap, uint32_t *n);

@@ -107,6 +107,9 @@ struct RunOut {
 // distinct (list variant, gap horizon) are built once, then one mining kernel
 // per motif runs on the same stream.
 thread_local std::vector<tm_kernel_info> g_kinfo;
+static_assert(TM_KMODE_COUNT == kCount && TM_KMODE_ENUM == kEnum && TM_KMODE_COUNT_PREFIX == kCountPfx &&
+                  TM_KMODE_RESUME == kResume && TM_KMODE_COUNT_SIB == kCountSib,
+              "tmotif.h kernel modes follow tmg::Mode");
 
 tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, const tm_run_opts *opts, int mode,
                     uint32_t *enum_dev, uint64_t cap, const uint64_t *roots_dev, uint64_t n_roots_list,
@@ -123,7 +126,12 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
     const DeviceGraph &d = g->d;
     const uint64_t m = d.m;
     g_info = tm_run_info{};
-    g_kinfo.assign(k, tm_kernel_info{});
+    {
+        tm_kernel_info none{};
+        none.carried_by = -1;
+        none.kernel_mode = TM_KMODE_NONE;
+        g_kinfo.assign(k, none);
+    }
     if (o.edge_id_offset + m > (1ull << 32)) return fail(TM_EINVAL, "edge_id_offset + m exceeds 2^32");
 
     MineParams base;
@@ -524,6 +532,7 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             g_info.grid_ctas = (uint32_t)grid;
             g_info.block_threads = threads;
             g_kinfo[i].grid_ctas = (uint32_t)grid;
+            g_kinfo[i].kernel_mode = kmode;
         }
         TM_CUDA_TRY(cudaEventRecord(evk[i], s));
     }
@@ -555,10 +564,12 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             out[i].count = host[(size_t)carrier[i] * kScratchWords + kPrefixBase + mos[i]->L];
             ki = tm_kernel_info{};
             ki.carried_by = carrier[i];
+            ki.kernel_mode = TM_KMODE_NONE;
         } else if (sib_of[i] >= 0) {   // sibling: the number of rows its carrier emitted
             out[i].count = host[(size_t)sib_of[i] * kScratchWords + kSibCount];
             ki = tm_kernel_info{};
             ki.carried_by = sib_of[i];
+            ki.kernel_mode = TM_KMODE_NONE;
         }
         for (int w = 0; w < kScratchWords; w++) out[i].stats[w] = h[w];
 #ifdef TM_PHASE_PROFILE

@@ -1186,8 +1186,13 @@ template <uint64_t CODE>
 struct MinBlocks<PlanC<CODE, false>, kCountPfx> : MinBlocks<PlanC<CODE, false>, kCount> {};
 template <uint64_t CODE>
 struct MinBlocks<PlanC<CODE, false>, kResume> : MinBlocks<PlanC<CODE, false>, kCount> {};
+#ifndef TM_MIN_BLOCKS_SIB
+#define TM_MIN_BLOCKS_SIB 0   // 0: as the counting kernel
+#endif
 template <uint64_t CODE>
-struct MinBlocks<PlanC<CODE, false>, kCountSib> : MinBlocks<PlanC<CODE, false>, kCount> {};
+struct MinBlocks<PlanC<CODE, false>, kCountSib> {
+    static constexpr int value = TM_MIN_BLOCKS_SIB ? TM_MIN_BLOCKS_SIB : MinBlocks<PlanC<CODE, false>, kCount>::value;
+};
 #ifndef TM_MIN_BLOCKS_ENUM
 #define TM_MIN_BLOCKS_ENUM 4
 #endif

@@ -55,9 +55,13 @@ class RunInfo(ctypes.Structure):
                 ("tail_ms", _f32), ("warp_busy", _f32)]
 
 
+# tm_kernel_info.kernel_mode (tmotif.h TM_KMODE_*)
+KMODE_NONE, KMODE_COUNT, KMODE_ENUM, KMODE_COUNT_PREFIX, KMODE_RESUME, KMODE_COUNT_SIB = -1, 0, 1, 4, 5, 6
+
+
 class KernelInfo(ctypes.Structure):
     _fields_ = [("mine_ms", _f32), ("tail_ms", _f32), ("warp_busy", _f32), ("grid_ctas", _u32),
-                ("shared_tasks", _u64), ("carried_by", _i32)]
+                ("shared_tasks", _u64), ("carried_by", _i32), ("kernel_mode", _i32)]
 
 
 _lib = None
@@ -345,7 +349,8 @@ def tm_last_kernel_info() -> list:
     buf = (KernelInfo * max(1, n.value))()
     _check(lib().tm_last_kernel_info(buf, n.value, ctypes.byref(n)))
     return [{"mine_ms": b.mine_ms, "tail_ms": b.tail_ms, "warp_busy": b.warp_busy, "grid_ctas": b.grid_ctas,
-             "shared_tasks": b.shared_tasks, "carried_by": b.carried_by} for b in buf[: n.value]]
+             "shared_tasks": b.shared_tasks, "carried_by": b.carried_by,
+             "kernel_mode": b.kernel_mode} for b in buf[: n.value]]
 
 
 def tm_census36(g: Graph, delta: int, fine=None, **opts) -> np.ndarray:

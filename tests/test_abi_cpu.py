@@ -97,4 +97,14 @@ def test_declared_struct_sizes_match_binding():
     assert T.RunInfo.shared_tasks.offset == 24
     assert ctypes.sizeof(T.KernelInfo) == 32 and T.KernelInfo.shared_tasks.offset == 16
     assert T.KernelInfo.carried_by.offset == 24
+    assert T.KernelInfo.kernel_mode.offset == 28
     assert ctypes.sizeof(T.SearchStats) == 8 * 13
+
+
+def test_kernel_mode_constants_match_header():
+    import re
+    txt = open(HEADER).read()
+    want = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define TM_KMODE_(\w+)\s+\(?(-?\d+)\)?", txt)}
+    assert want == {"NONE": -1, "COUNT": 0, "ENUM": 1, "COUNT_PREFIX": 4, "RESUME": 5, "COUNT_SIB": 6}
+    for k, v in want.items():
+        assert getattr(T, "KMODE_" + k) == v

@@ -639,6 +639,9 @@ def test_sibling_rows_and_resume():
     kin = T.tm_last_kernel_info()
     assert kin[1]["carried_by"] == 0 and kin[1]["grid_ctas"] == 0   # TRI: rows of the 4-cycle kernel
     assert kin[2]["grid_ctas"] > 0                                   # the diamond's resume kernel ran
+    assert [x["kernel_mode"] for x in kin] == [T.KMODE_COUNT_SIB, T.KMODE_NONE, T.KMODE_RESUME]
+    T.tm_count_multi(g, mos, fuse=1)
+    assert [x["kernel_mode"] for x in T.tm_last_kernel_info()] == [T.KMODE_COUNT] * 3
     # dense bursts: thousands of triangles and diamonds (the row buffer holds them all)
     for core in (30, 40):
         s1, d1, t1, n1 = synth.burst_graph(11, n=2000, m_bg=20000, bursts=2, core=core, burst_len=1800)
