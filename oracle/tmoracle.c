@@ -36,7 +36,8 @@
  *      we scan the shorter list, ties -> N_in(v_G).  Results do not depend
  *      on the choice; the instrumentation counters do.
  *   Q9 a motif edge after the first that touches no earlier motif vertex
- *      (Alg. 1's "Both u_G, v_G not mapped" branch) is rejected.
+ *      takes Alg. 1's "Both u_G, v_G not mapped" branch: its
+ *      candidates are all later edges of the time-sorted edge list.
  *
  * Generalized query:
  *   labels   vertex/edge labels are small integers (unlabeled = 0); a motif
@@ -345,15 +346,20 @@ static void search_level(tmo_ctx *c) {
     uint64_t root = c->eStack[0], prev = c->eStack[c->depth - 1];
 
     /* GetCandidateEdgeList */
-    const uint64_t *list; uint64_t len;
-    if (uG >= 0 && vG >= 0) {
+    const uint64_t *list = NULL; uint64_t len;
+    if (uG < 0 && vG < 0) {
+        /* AllEdges: a motif edge that touches no earlier motif
+         * vertex takes its candidates from the whole time-sorted edge list,
+         * whose p-th entry is sorted edge p (list == NULL below) */
+        len = g->m;
+    } else if (uG >= 0 && vG >= 0) {
         uint64_t lo_ = g->out_off[uG + 1] - g->out_off[uG];
         uint64_t li_ = g->in_off[vG + 1] - g->in_off[vG];
         if (lo_ < li_) { list = g->out_e + g->out_off[uG]; len = lo_; }
         else           { list = g->in_e + g->in_off[vG];   len = li_; }
     } else if (uG >= 0) {
         list = g->out_e + g->out_off[uG]; len = g->out_off[uG + 1] - g->out_off[uG];
-    } else {  /* vG >= 0: validation (Q9) rules out the AllEdges branch */
+    } else {  /* vG >= 0 */
         list = g->in_e + g->in_off[vG]; len = g->in_off[vG + 1] - g->in_off[vG];
     }
     c->st.nodes[c->depth]++;
@@ -362,8 +368,8 @@ static void search_level(tmo_ctx *c) {
 
     int64_t troot = g->t[root], tprev = g->t[prev];
     int64_t fine = q->fine[eM - 1];  /* δ_{eM} between motif edges eM and eM+1 (1-based) */
-    for (uint64_t p = first_after(g, list, len, prev); p < len; p++) {
-        uint64_t e = list[p];
+    for (uint64_t p = list ? first_after(g, list, len, prev) : prev + 1; p < len; p++) {
+        uint64_t e = list ? list[p] : p;
         if (g->t[e] - troot > q->delta) break;   /* time(e) > t' : Backtrack */
         if (g->t[e] - tprev > fine) break;        /* fine-grained bound */
         c->st.window_sum++;
@@ -394,16 +400,13 @@ static void mine_root(tmo_ctx *c, uint64_t r) {
 }
 
 /* Motif validation: 1 <= L <= TMO_MAXL, ids < TMO_MAXV, u != v, δ >= 0,
- * δ_i >= 0, and (Q9) every edge after the first shares a vertex with an
- * earlier edge. */
+ * δ_i >= 0.  A motif edge that shares no vertex with the earlier ones
+ * (prefix-disconnected) is searched with the AllEdges list (Q9). */
 static int validate(uint32_t L, const uint32_t *mu, const uint32_t *mv, int64_t delta, const int64_t *fine) {
     if (L < 1 || L > TMO_MAXL || delta < 0) return TMO_EINVAL;
-    int seen[TMO_MAXV] = {0};
     for (uint32_t i = 0; i < L; i++) {
         if (mu[i] >= TMO_MAXV || mv[i] >= TMO_MAXV || mu[i] == mv[i]) return TMO_EINVAL;
         if (fine && i + 1 < L && fine[i] < 0) return TMO_EINVAL;
-        if (i > 0 && !seen[mu[i]] && !seen[mv[i]]) return TMO_EUNSUPPORTED;
-        seen[mu[i]] = seen[mv[i]] = 1;
     }
     return TMO_OK;
 }

@@ -273,9 +273,7 @@ def test_multithreaded_equals_single():
 
 def test_validation():
     g = oracle.Graph(np.array([0], np.uint32), np.array([1], np.uint32), np.array([0], np.int64), 2)
-    with pytest.raises(oracle.OracleError) as ei:
-        g.mine([(0, 1), (2, 3)], 5)          # prefix-disconnected (Q9)
-    assert ei.value.code == oracle.EUNSUPPORTED
+    assert g.mine([(0, 1), (2, 3)], 5)["count"] == 0   # prefix-disconnected: AllEdges (Q9)
     with pytest.raises(oracle.OracleError):
         g.mine([(0, 0)], 5)                  # motif self-loop
     with pytest.raises(oracle.OracleError):
@@ -392,3 +390,40 @@ def test_constraint_invariants():
         og.mine(M.TRI, 30, anti=[(0, 7, 0, 5)])
     with pytest.raises(oracle.OracleError):
         og.mine(M.TRI, 30, anti=[(0, 1, 3, 5)])
+
+
+# ------------------------------------------------ prefix-disconnected motifs (Q9)
+DISCONNECTED = [[(0, 1), (2, 3)], [(0, 1), (2, 3), (1, 2)], [(0, 1), (2, 3), (3, 0)],
+                [(0, 1), (2, 3), (4, 5)], [(0, 1), (1, 2), (3, 4), (4, 0)], [(0, 1), (2, 1), (3, 4)]]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_disconnected_motifs_vs_brute(seed):
+    """A motif edge that touches no earlier motif vertex takes its candidates
+    from all later edges (Alg. 1's AllEdges branch)."""
+    rng = random.Random(900 + seed)
+    for k in range(24):
+        motif = DISCONNECTED[k % len(DISCONNECTED)]
+        src, dst, t, n = synth.tiny_graph(seed * 100 + k, n=rng.randint(4, 9), m=rng.randint(0, 40), tmax=30)
+        delta = rng.choice([0, 3, 10, INF])
+        fine = random_fine(rng, len(motif))
+        rows, n_total = orows(src, dst, t, n, motif, delta, fine)
+        assert rows == brute(src, dst, t, motif, delta, fine), (motif, delta, fine)
+
+
+def test_disjoint_edge_pairs_closed_form():
+    """[(0,1), (2,3)] with δ = ∞ counts the vertex-disjoint pairs of non-loop
+    edges: C(m,2) − Σ_v C(d_v,2) + Σ_{a<b} C(c_ab,2) by inclusion–exclusion
+    (d_v = edges at v, c_ab = edges between a and b in either direction)."""
+    from math import comb
+    for seed in range(6):
+        src, dst, t, n = synth.tiny_graph(4000 + seed, n=12, m=150, tmax=1000)
+        keep = src != dst
+        src, dst, t = src[keep], dst[keep], t[keep]
+        deg = np.bincount(np.concatenate([src, dst]), minlength=n)
+        pairs = {}
+        for a, b in zip(src.tolist(), dst.tolist()):
+            key = (min(a, b), max(a, b))
+            pairs[key] = pairs.get(key, 0) + 1
+        want = comb(len(src), 2) - sum(comb(int(d), 2) for d in deg) + sum(comb(c, 2) for c in pairs.values())
+        assert ocount(src, dst, t, n, [(0, 1), (2, 3)], INF) == want
