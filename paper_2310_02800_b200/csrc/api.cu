@@ -378,18 +378,22 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
     TM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int threads = kWarpsPerBlock * 32;
     // sibling rows: one region per sibling motif (cap rows of L_b edge ids)
+    // (a sibling nobody resumes from is only counted: no rows, cap 0)
     std::vector<uint32_t *> sib_region(k, nullptr);
+    std::vector<char> rows_needed(k, 0);
+    for (uint32_t d = 0; d < k; d++)
+        if (resume_of[d] >= 0) rows_needed[resume_of[d]] = 1;
     {
         uint64_t words = 0;
         sib_cap = std::min<uint64_t>(std::max<uint64_t>(base.n_roots, 1u << 16), 1u << 22);
         for (uint32_t b = 0; b < k; b++)
-            if (sib_of[b] >= 0) words += sib_cap * mos[b]->L;
+            if (sib_of[b] >= 0 && rows_needed[b]) words += sib_cap * mos[b]->L;
         if (words) {
             TM_CUDA_TRY(dev_alloc((void **)&sib_rows, words * sizeof(uint32_t), s));
             fr.v.push_back(sib_rows);
             uint64_t off = 0;
             for (uint32_t b = 0; b < k; b++)
-                if (sib_of[b] >= 0) {
+                if (sib_of[b] >= 0 && rows_needed[b]) {
                     sib_region[b] = sib_rows + off;
                     off += sib_cap * mos[b]->L;
                 }
@@ -418,7 +422,7 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
                 p.sib_level = sib_K[b];
                 p.sib_vtx = sib_vtx[b];
                 p.sib_rows = sib_region[b];
-                p.sib_cap = (uint32_t)sib_cap;
+                p.sib_cap = rows_needed[b] ? (uint32_t)sib_cap : 0u;
             }
         const bool resuming = resume_of[i] >= 0;
         if (resuming) {   // continue from sibling b's rows
