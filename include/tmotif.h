@@ -14,7 +14,7 @@
  * φ(u_i) = src(e_i), φ(v_i) = dst(e_i).  The library counts the
  * matches or enumerates them into a caller buffer ("enumerated or
  * counted").  DESIGN.md lists every reading of the paper this encodes
- * (ties Q1, inclusive bounds Q2, self-loops Q4, unsupported motifs Q9 ...).
+ * (ties Q1, inclusive bounds Q2, self-loops Q4, all-edges candidates Q9 ...).
  *
  * Conventions
  *  - Every call returns tm_status; TM_OK = 0.  No C++ exception crosses the
@@ -45,7 +45,7 @@ typedef enum {
     TM_EINVAL = 1,        /* invalid argument (message says which)                  */
     TM_ENOMEM = 2,        /* device or host allocation failed                       */
     TM_ECUDA = 3,         /* a CUDA runtime error (message carries cudaGetErrorString) */
-    TM_EUNSUPPORTED = 4,  /* motif outside the supported set (prefix-disconnected, Q9) */
+    TM_EUNSUPPORTED = 4,  /* feature combination not supported (see tm_motif_create) */
     TM_TRUNCATED = 5      /* tm_enumerate: more matches than buffer rows            */
 } tm_status;
 
@@ -104,9 +104,14 @@ tm_status tm_graph_sorted_edges(const tm_graph *g, uint32_t *src, uint32_t *dst,
  *              t(e_{i+1}) (0-based gaps), each >= 0 or TM_DELTA_INF
  * Ownership: inputs copied; library owns *out until tm_motif_destroy.
  * Errors: TM_EINVAL (L out of range, mu[i] == mv[i] (motif self-loop),
- * label >= 64, more than TM_MAX_VERTICES vertices, δ < 0, δ_i < 0);
- * TM_EUNSUPPORTED when an edge after the first touches no earlier motif
- * vertex (Algorithm 1's all-edges candidate list; reading Q9). */
+ * label >= 64, more than TM_MAX_VERTICES vertices, δ < 0, δ_i < 0).
+ * A motif edge after the first that touches no earlier motif vertex
+ * ("prefix-disconnected") takes its candidates from all later edges of the
+ * time-sorted edge list (Algorithm 1's AllEdges branch; reading
+ * Q9): such motifs run a thread-per-root search kernel (TM_KMODE_DFS) for
+ * tm_count / tm_enumerate / tm_count_roots / tm_count_multi, and return
+ * TM_EUNSUPPORTED with labels, anti-edges, tm_search_stats_run or
+ * tm_motif_specialise. */
 tm_status tm_motif_create(uint32_t L, const uint32_t *mu, const uint32_t *mv, int64_t delta,
                           const int64_t *fine, tm_motif **out);
 
@@ -266,6 +271,7 @@ typedef struct {
 #define TM_KMODE_COUNT_PREFIX 4 /* count that also counts carried prefix motifs */
 #define TM_KMODE_RESUME 5       /* count resumed from the sibling rows of another kernel */
 #define TM_KMODE_COUNT_SIB 6    /* count that also writes a carried sibling motif's matches as rows */
+#define TM_KMODE_DFS 7          /* thread-per-root search of a prefix-disconnected motif (count / enumerate / roots) */
 
 /* Copies min(cap, n) entries to out (host); *n = number of kernels. */
 tm_status tm_last_kernel_info(tm_kernel_info *out, uint32_t cap, uint32_t *n);

@@ -115,8 +115,12 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
                     uint32_t *enum_dev, uint64_t cap, const uint64_t *roots_dev, uint64_t n_roots_list,
                     unsigned long long *root_counts_dev, RunOut *out) {
     if (!g || !mos || k == 0) return fail(TM_EINVAL, "null graph or motif");
-    for (uint32_t i = 0; i < k; i++)
+    for (uint32_t i = 0; i < k; i++) {
         if (!mos[i]) return fail(TM_EINVAL, "null motif");
+        if (mos[i]->disconnected && (mos[i]->constrained() || mode == kStats))
+            return fail(TM_EUNSUPPORTED, "prefix-disconnected motifs (Q9) support count / enumerate / per-root "
+                                         "counts without labels or anti-edges");
+    }
     tm_run_opts o;
     tm_run_opts_default(&o);
     if (opts) o = *opts;
@@ -187,7 +191,7 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         // window-end ranks (build_hrank) for the levels whose list is anchored at
         // the previous edge and bounded by a gap horizon.  The instrumentation
         // run (kStats) does not use them.
-        if (!TM_HRANK || mode == kStats) continue;
+        if (!TM_HRANK || mode == kStats || mo->disconnected) continue;
         Shape sh{};
         sh.L = (int)mo->L;
         for (uint32_t j = 0; j < mo->L; j++) { sh.u[j] = mo->u[j]; sh.v[j] = mo->v[j]; }
@@ -218,7 +222,9 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             for (uint32_t j = 0; j < mo->L; j++) { sh.u[j] = mo->u[j]; sh.v[j] = mo->v[j]; }
             return sh;
         };
-        auto plain = [](const tm_motif *mo) { return !mo->constrained() && !mo->rtc_fn[kCount]; };
+        auto plain = [](const tm_motif *mo) {
+            return !mo->constrained() && !mo->rtc_fn[kCount] && !mo->disconnected;
+        };
         for (uint32_t b = 0; b < k; b++) {   // B: a sibling of a launched motif A
             const tm_motif *mb = mos[b];
             if (!plain(mb) || mb->L < 2) continue;
@@ -287,11 +293,11 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
         for (uint32_t a = 0; a < k; a++) {
             const uint32_t i = order[a];
             const tm_motif *mi = mos[i];
-            if (mi->constrained() || sib_of[i] >= 0 || resume_of[i] >= 0) continue;
+            if (mi->constrained() || mi->disconnected || sib_of[i] >= 0 || resume_of[i] >= 0) continue;
             for (uint32_t b = 0; b < a && carrier[i] < 0; b++) {
                 const uint32_t j = order[b];
                 const tm_motif *mj = mos[j];
-                if (carrier[j] >= 0 || sib_of[j] >= 0 || resume_of[j] >= 0 || mj->constrained() ||
+                if (carrier[j] >= 0 || sib_of[j] >= 0 || resume_of[j] >= 0 || mj->constrained() || mj->disconnected ||
                     mj->rtc_fn[kCount] || mj->L <= mi->L ||
                     mj->delta != mi->delta)
                     continue;
@@ -463,7 +469,15 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
                     p.HR[j] = hwhich[i][j] >= 0 ? hrbuf + (size_t)hwhich[i][j] * m : nullptr;
             }
         }
-        if (p.n_roots > 0) {
+        if (p.n_roots > 0 && mo->disconnected) {   // two new vertices at one level: dfs.cu
+            uint32_t grid = 0;
+            TM_CUDA_TRY(launch_mine_dfs(p, mode, sms, s, &grid));
+            g_info.launches++;
+            g_info.grid_ctas = grid;
+            g_info.block_threads = 256;
+            g_kinfo[i].grid_ctas = grid;
+            g_kinfo[i].kernel_mode = TM_KMODE_DFS;
+        } else if (p.n_roots > 0) {
             bool spec = false;
             // a runtime-specialised kernel (tm_motif_specialise) first, then the
             // build-time catalog, then the generic kernel
@@ -710,9 +724,7 @@ tm_status tm_motif_create(uint32_t L, const uint32_t *mu, const uint32_t *mv, in
         if (mu[i] >= 64 || mv[i] >= 64) return fail(TM_EINVAL, "motif vertex label >= 64");
         if (mu[i] == mv[i]) return fail(TM_EINVAL, "motif self-loop");
         const bool seen_u = label[mu[i]] >= 0, seen_v = label[mv[i]] >= 0;
-        if (i > 0 && !seen_u && !seen_v)
-            return fail(TM_EUNSUPPORTED, "motif edge " + std::to_string(i) +
-                                             " touches no earlier motif vertex (prefix-disconnected, reading Q9)");
+        if (i > 0 && !seen_u && !seen_v) mo.disconnected = true;   // AllEdges candidates (Q9)
         // relabel by first appearance (u before v)
         if (!seen_u) label[mu[i]] = nv++;
         if (!seen_v) label[mv[i]] = nv++;
@@ -786,13 +798,14 @@ tm_status tm_graph_set_labels(tm_graph *g, const int32_t *vlabels, const int32_t
 
 tm_status tm_motif_specialised(const tm_motif *mo, int *sp) {
     if (!mo || !sp) return fail(TM_EINVAL, "null argument");
-    *sp = mo->rtc_fn[kCount] || (is_specialised(mo->code) && !mo->constrained()) ? 1 : 0;
+    *sp = !mo->disconnected && (mo->rtc_fn[kCount] || (is_specialised(mo->code) && !mo->constrained())) ? 1 : 0;
     return TM_OK;
 }
 
 tm_status tm_motif_specialise(tm_motif *mo) {
     g_err.clear();
     if (!mo) return fail(TM_EINVAL, "null motif");
+    if (mo->disconnected) return fail(TM_EUNSUPPORTED, "a prefix-disconnected motif (Q9) runs the dfs kernel");
     if (is_specialised(mo->code) && !mo->constrained()) return TM_OK;   // in the build-time catalog
     for (int mode : {(int)kCount, (int)kEnum}) {
         RtcKernel k;

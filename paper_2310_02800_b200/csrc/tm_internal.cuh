@@ -149,6 +149,7 @@ struct tm_motif {
     uint32_t n_anti = 0;
     uint8_t anti_u[TM_MAX_ANTI] = {}, anti_v[TM_MAX_ANTI] = {}, anti_attach[TM_MAX_ANTI] = {};
     int64_t anti_window[TM_MAX_ANTI] = {};
+    bool disconnected = false;   // some edge after the first touches no earlier vertex (Q9): dfs.cu
     void *rtc_fn[2] = {nullptr, nullptr};   // tm_motif_specialise: count / enumerate kernels (CUfunction)
     int rtc_smem[2] = {0, 0};               // their shared memory per warp (bytes)
     bool constrained() const {
@@ -271,6 +272,8 @@ struct CensusParams {
 
 #ifndef __CUDACC_RTC__
 cudaError_t launch_census36(const CensusParams &p, int grid, cudaStream_t s);
+// prefix-disconnected motifs (dfs.cu): thread-per-root search, modes kCount / kEnum / kRoots
+cudaError_t launch_mine_dfs(const MineParams &p, int mode, int sms, cudaStream_t s, uint32_t *grid_out);
 
 using MineKernel = void (*)(MineParams);
 

@@ -56,7 +56,7 @@ class RunInfo(ctypes.Structure):
 
 
 # tm_kernel_info.kernel_mode (tmotif.h TM_KMODE_*)
-KMODE_NONE, KMODE_COUNT, KMODE_ENUM, KMODE_COUNT_PREFIX, KMODE_RESUME, KMODE_COUNT_SIB = -1, 0, 1, 4, 5, 6
+KMODE_NONE, KMODE_COUNT, KMODE_ENUM, KMODE_COUNT_PREFIX, KMODE_RESUME, KMODE_COUNT_SIB, KMODE_DFS = -1, 0, 1, 4, 5, 6, 7
 
 
 class KernelInfo(ctypes.Structure):

@@ -42,8 +42,11 @@ def test_motif_validation_and_specialisation():
     assert T.Motif([(7, 3), (3, 9), (9, 7)], 3600).specialised          # relabelled TRI
     assert T.Motif([(0, 1), (1, 2), (2, 3), (3, 0)], 10).specialised    # C4
     assert not T.Motif([(0, 1), (1, 0), (1, 2), (2, 1)], 10).specialised  # generic runtime plan
+    # prefix-disconnected (Q9): accepted, searched by the thread-per-root kernel, not specialisable
+    mo = T.Motif([(0, 1), (2, 3)], 10)
+    assert not mo.specialised
     with pytest.raises(T.TMotifError) as e:
-        T.Motif([(0, 1), (2, 3)], 10)
+        mo.specialise()
     assert e.value.status == T.TM_EUNSUPPORTED
     for bad in ([(0, 0)], [], [(0, 1)] * 7, [(0, 64)]):
         with pytest.raises(T.TMotifError) as e:
@@ -105,6 +108,6 @@ def test_kernel_mode_constants_match_header():
     import re
     txt = open(HEADER).read()
     want = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define TM_KMODE_(\w+)\s+\(?(-?\d+)\)?", txt)}
-    assert want == {"NONE": -1, "COUNT": 0, "ENUM": 1, "COUNT_PREFIX": 4, "RESUME": 5, "COUNT_SIB": 6}
+    assert want == {"NONE": -1, "COUNT": 0, "ENUM": 1, "COUNT_PREFIX": 4, "RESUME": 5, "COUNT_SIB": 6, "DFS": 7}
     for k, v in want.items():
         assert getattr(T, "KMODE_" + k) == v

@@ -663,3 +663,43 @@ def test_sibling_rows_and_resume():
     exp = [og2.mine(M.get(nm), 3600, ff)["count"] for nm, ff in specs]
     assert exp[1] > 65536
     assert T.tm_count_multi(g2, [T.Motif(M.get(nm), 3600, ff) for nm, ff in specs]) == exp
+
+
+# ------------------------------------------- prefix-disconnected motifs (Q9)
+DISCONNECTED = [[(0, 1), (2, 3)], [(0, 1), (2, 3), (1, 2)], [(0, 1), (2, 3), (3, 0)],
+                [(0, 1), (2, 3), (4, 5)], [(0, 1), (1, 2), (3, 4), (4, 0)], [(0, 1), (2, 1), (3, 4)]]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_disconnected_motifs_vs_oracle(seed):
+    """AllEdges levels on the thread-per-root kernel: counts,
+    enumerations and per-root counts equal the oracle's."""
+    rng = random.Random(700 + seed)
+    for k in range(18):
+        motif = DISCONNECTED[k % len(DISCONNECTED)]
+        src, dst, t, n = synth.tiny_graph(seed * 100 + k, n=rng.randint(4, 12), m=rng.randint(0, 80), tmax=40)
+        delta = rng.choice([0, 3, 10, INF])
+        check_case(src, dst, t, n, motif, delta, random_fine(rng, len(motif)), stats=False)
+    # a bigger graph: several thousand roots, long all-edge windows
+    src, dst, t, n = synth.config_graph("C1", m=3000)
+    for motif, delta in (([(0, 1), (2, 3)], 600), ([(0, 1), (2, 3), (1, 2)], 7200), ([(0, 1), (1, 2), (3, 4), (4, 0)], 20000)):
+        c = check_case(src, dst, t, n, motif, delta, None, rows=seed == 0, stats=False)
+        assert c > 0
+
+
+def test_disconnected_in_multi_and_errors():
+    src, dst, t, n = synth.config_graph("C1", m=2000)
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    specs = [([(0, 1), (2, 3)], 7200), (M.P3, 7200), ([(0, 1), (2, 3), (1, 2)], 7200), (M.TRI, 7200)]
+    exp = [og.mine(mm, d)["count"] for mm, d in specs]
+    assert T.tm_count_multi(g, [T.Motif(mm, d) for mm, d in specs]) == exp
+    kin = T.tm_last_kernel_info()
+    assert kin[0]["kernel_mode"] == T.KMODE_DFS and kin[2]["kernel_mode"] == T.KMODE_DFS
+    mo = T.Motif([(0, 1), (2, 3)], 600)
+    with pytest.raises(T.TMotifError) as e:
+        T.tm_search_stats_run(g, mo)
+    assert e.value.status == T.TM_EUNSUPPORTED
+    with pytest.raises(T.TMotifError) as e:
+        T.tm_count(g, T.Motif([(0, 1), (2, 3)], 600, vlabels={0: 1}))
+    assert e.value.status == T.TM_EUNSUPPORTED
