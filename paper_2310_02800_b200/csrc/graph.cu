@@ -89,35 +89,57 @@ __global__ void k_horizon_ends(const int64_t *__restrict__ T, uint64_t m, int64_
     }
 }
 
-__global__ void __launch_bounds__(kHB) k_horizon(const int64_t *__restrict__ T, uint64_t m, int64_t d,
-                                                 const uint64_t *__restrict__ ends, uint32_t *__restrict__ H) {
+// kHB / kHEpt threads per block, kHEpt edges each (strided for coalescing):
+// the kHEpt branch-free binary searches of a thread are independent, so their
+// shared-memory loads overlap (the kernel is bound by that latency chain).
+#ifndef TM_HORIZON_EPT
+#define TM_HORIZON_EPT 4
+#endif
+constexpr int kHEpt = TM_HORIZON_EPT;
+constexpr int kHThreads = kHB / kHEpt;
+
+__global__ void __launch_bounds__(kHThreads) k_horizon(const int64_t *__restrict__ T, uint64_t m, int64_t d,
+                                                       const uint64_t *__restrict__ ends, uint32_t *__restrict__ H) {
     __shared__ int64_t st[kHStage];
     const uint64_t e0 = (uint64_t)blockIdx.x * kHB;
-    const uint64_t e = e0 + threadIdx.x;
     const uint64_t elast = min(e0 + kHB, m) - 1;
     const uint64_t lo = ends[2 * blockIdx.x], hi = ends[2 * blockIdx.x + 1];   // answers lie in [lo, hi]
     const uint64_t span = hi - lo + 1;
+    int64_t te[kHEpt];
+#pragma unroll
+    for (int j = 0; j < kHEpt; j++) {
+        const uint64_t e = e0 + threadIdx.x + (uint64_t)j * kHThreads;
+        te[j] = e <= elast ? T[e] : 0;
+    }
     if (span <= kHStage) {
-        for (uint64_t i = threadIdx.x; i < span; i += kHB) st[i] = T[lo + i];
+        for (uint64_t i = threadIdx.x; i < span; i += kHThreads) st[i] = T[lo + i];
         __syncthreads();
-        if (e <= elast) {
-            const int64_t te = T[e];
-            uint64_t r;
-            if (d == TM_DELTA_INF || te > INT64_MAX - d) {
-                r = m - 1;
-            } else {
-                const int64_t key = te + d;   // st[0] = T[H(e0)] <= key
-                uint32_t a = 0, b = (uint32_t)span;
-                while (a < b) {
-                    uint32_t mid = (a + b) >> 1;
-                    if (st[mid] > key) b = mid; else a = mid + 1;
-                }
-                r = lo + a - 1;
-            }
-            H[e] = (uint32_t)r;
+        // last index with st[idx] <= key; st[0] = T[H(e0)] <= key for every e >= e0
+        uint32_t base[kHEpt];
+        int64_t key[kHEpt];
+#pragma unroll
+        for (int j = 0; j < kHEpt; j++) {
+            base[j] = 0;
+            key[j] = (d == TM_DELTA_INF || te[j] > INT64_MAX - d) ? INT64_MAX : te[j] + d;
         }
-    } else if (e <= elast) {
-        H[e] = (uint32_t)horizon_one(T, m, d, e);
+        for (uint32_t len = (uint32_t)span; len > 1;) {
+            const uint32_t half = len >> 1;
+#pragma unroll
+            for (int j = 0; j < kHEpt; j++)
+                if (st[base[j] + half] <= key[j]) base[j] += half;
+            len -= half;
+        }
+#pragma unroll
+        for (int j = 0; j < kHEpt; j++) {
+            const uint64_t e = e0 + threadIdx.x + (uint64_t)j * kHThreads;
+            if (e <= elast) H[e] = (uint32_t)(key[j] == INT64_MAX ? m - 1 : lo + base[j]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kHEpt; j++) {
+            const uint64_t e = e0 + threadIdx.x + (uint64_t)j * kHThreads;
+            if (e <= elast) H[e] = (uint32_t)horizon_one(T, m, d, e);
+        }
     }
 }
 
@@ -385,7 +407,7 @@ cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, uint
     if (!d.m) return cudaSuccess;
     const uint64_t nb = (d.m + kHB - 1) / kHB;
     k_horizon_ends<<<grid_for(2 * nb), 256, 0, s>>>(d.t, d.m, delta, scratch);
-    k_horizon<<<(unsigned)nb, kHB, 0, s>>>(d.t, d.m, delta, scratch, H);
+    k_horizon<<<(unsigned)nb, kHThreads, 0, s>>>(d.t, d.m, delta, scratch, H);
     return cudaGetLastError();
 }
 
