@@ -442,6 +442,38 @@ __device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, co
 
 constexpr int kHrUnroll = 4;   // edges per thread in flight (independent load chains)
 
+// Warp-cooperative long path (TM_HRANK_WARP_LONG): the lanes whose window
+// runs past the first sector are served one at a time by the whole warp,
+// 32 records per coalesced load, up to kHrWarpIters loads, then the gallop.
+// Must be reached by all 32 lanes (no lane may have left the loop).
+#ifndef TM_HRANK_WARP_LONG
+#define TM_HRANK_WARP_LONG 0   // measured slower: 3.86 vs 2.66 ms (profiles/r01_experiments.md)
+#endif
+constexpr int kHrWarpIters = 4;
+__device__ __forceinline__ uint32_t hrank_long_warp(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ vtx,
+                                                    const uint32_t *__restrict__ offs, uint64_t e, uint32_t a,
+                                                    uint32_t lim, uint32_t ans) {
+    const int lane = threadIdx.x & 31;
+    unsigned need = __ballot_sync(0xffffffffu, ans == 0xFFFFFFFFu);
+    while (need) {
+        const int src = __ffs(need) - 1;
+        need &= need - 1;
+        const uint64_t es = __shfl_sync(0xffffffffu, e, src);
+        const uint32_t as = __shfl_sync(0xffffffffu, a, src), ls = __shfl_sync(0xffffffffu, lim, src);
+        const uint32_t last = __ldg(offs + vtx[es] + 1) - 1;   // the list's sentinel
+        uint32_t res = 0xFFFFFFFFu, pos = as;
+        for (int it = 0; it < kHrWarpIters && res == 0xFFFFFFFFu; it++, pos += 32) {
+            const uint32_t q = pos + lane;
+            const bool over = q > last || (uint32_t)(__ldg(rec + q) >> 32) > ls;
+            const unsigned m = __ballot_sync(0xffffffffu, over);
+            if (m) res = pos + __ffs(m) - 1;
+        }
+        if (res == 0xFFFFFFFFu && lane == src) res = hrank_long(rec, vtx, offs, es, pos, ls);
+        if (lane == src) ans = res;
+    }
+    return ans;
+}
+
 // R: window-end ranks (u32 per edge), or W: window descriptors {start, end,
 // H[e], 0} (uint4 per edge) when W != nullptr
 __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ rank,
@@ -449,7 +481,10 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
                                                const uint32_t *__restrict__ H, uint64_t m, uint32_t *__restrict__ R,
                                                uint4 *__restrict__ W) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < m; e0 += stride * kHrUnroll) {
+    // warp-uniform trip count (the warp long path needs all 32 lanes)
+    const uint64_t lane0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+    for (uint64_t w0 = lane0; w0 < m; w0 += stride * kHrUnroll) {
+        const uint64_t e0 = w0 + (threadIdx.x & 31u);
         uint32_t lim[kHrUnroll], b[kHrUnroll];
         ulonglong2 x0[kHrUnroll], x1[kHrUnroll];
 #pragma unroll
@@ -469,7 +504,9 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
 #pragma unroll
         for (int u = 0; u < kHrUnroll; u++) {
             const uint64_t e = e0 + u * stride;
+#if !TM_HRANK_WARP_LONG
             if (e >= m) break;
+#endif
             const uint32_t a = b[u] & ~3u;
             const uint32_t id[4] = {(uint32_t)(x0[u].x >> 32), (uint32_t)(x0[u].y >> 32), (uint32_t)(x1[u].x >> 32),
                                     (uint32_t)(x1[u].y >> 32)};
@@ -477,7 +514,13 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
 #pragma unroll
             for (int k = 3; k >= 0; --k)
                 if (a + k >= b[u] && id[k] > lim[u]) ans = a + k;
+#if TM_HRANK_WARP_LONG
+            if (e >= m) ans = 0;   // no edge: not a long-path request
+            ans = hrank_long_warp(rec, vtx, offs, e, a + 4, lim[u], ans);
+            if (e >= m) continue;
+#else
             if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, vtx, offs, e, a + 4, lim[u]);
+#endif
             if (W) W[e] = make_uint4(b[u], ans, lim[u], 0u);
             else R[e] = ans;
         }
