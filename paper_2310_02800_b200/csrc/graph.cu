@@ -423,10 +423,13 @@ namespace {
 // are δ-short and every list ends in an id-0xFFFFFFFF sentinel.
 // window end of edge e when it lies beyond the first sector: gallop from
 // a (the first unread position), capped at the list's sentinel
+#ifndef TM_HR_STEP0
+#define TM_HR_STEP0 4   // first gallop step (records)
+#endif
 __device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ vtx,
                                             const uint32_t *__restrict__ offs, uint64_t e, uint32_t a, uint32_t lim) {
     const uint32_t last = __ldg(offs + vtx[e] + 1) - 1;
-    uint32_t lo = a, step = 4, hi = min(lo + 3, last);
+    uint32_t lo = a, step = TM_HR_STEP0, hi = min(lo + TM_HR_STEP0 - 1, last);
     while ((uint32_t)(__ldg(rec + hi) >> 32) <= lim) {
         lo = hi + 1;
         step <<= 1;
@@ -440,7 +443,10 @@ __device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, co
     return lo;
 }
 
-constexpr int kHrUnroll = 4;   // edges per thread in flight (independent load chains)
+#ifndef TM_HR_UNROLL
+#define TM_HR_UNROLL 4
+#endif
+constexpr int kHrUnroll = TM_HR_UNROLL;   // edges per thread in flight (independent load chains)
 
 // Warp-cooperative long path (TM_HRANK_WARP_LONG): the lanes whose window
 // runs past the first sector are served one at a time by the whole warp,
