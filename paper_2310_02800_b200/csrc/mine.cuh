@@ -360,6 +360,9 @@ struct PlanR {
     template <int I> __device__ __forceinline__ bool pairk() const { return pairk_[I]; }
 };
 
+#ifndef TM_SIB_LAZY_EH
+#define TM_SIB_LAZY_EH 1
+#endif
 // ------------------------------------------------------- shared-memory layout
 // Per warp, per level l = 1..kL-1, a structure of arrays of kCap tasks:
 //   [0] lo  [1] up  [2] hi  [3 .. 3+S) φ  [.. +l) matched edge ids  [+1] root slot (kRoots)
@@ -373,6 +376,11 @@ struct Layout {
     __host__ __device__ static constexpr bool keh(int l, int k) {
         return k < l && (MODE == kEnum || MODE == kStats || (MODE == kCountSib && l <= kSibLevel) ||
                          Plan::keep_eh(l, k));
+    }
+    // matched ids a level-l expansion loads per candidate: the sibling rows'
+    // extra ids at kSibLevel are read from shared memory only for a row
+    __host__ __device__ static constexpr bool keh_load(int l, int k) {
+        return keh(l, k) && !(TM_SIB_LAZY_EH && MODE == kCountSib && l == kSibLevel && k < l && !Plan::keep_eh(l, k));
     }
     __host__ __device__ static constexpr bool khi(int l) { return MODE == kStats || Plan::keep_hi(l); }
     __host__ __device__ static constexpr int phi(int l, int k) {
@@ -906,7 +914,7 @@ struct Warp {
             if constexpr (Lay::khi(LV)) hi = fld<LV, Lay::hi(LV)>()[jt];
             sfor<LV>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
-                if constexpr (Lay::keh(LV, k)) eh[k] = fld<LV, Lay::eh(LV, k)>()[jt];
+                if constexpr (Lay::keh_load(LV, k)) eh[k] = fld<LV, Lay::eh(LV, k)>()[jt];
                 else eh[k] = 0u;
             });
             if constexpr (MODE == kRoots) rslot = fld<LV, Lay::rs(LV)>()[jt];
@@ -936,8 +944,10 @@ struct Warp {
                         const unsigned long long row = base + __popc(smask & lanemask_lt());
                         if (row < p.sib_cap) {
                             uint32_t *dst = p.sib_rows + row * (LV + 1);
-#pragma unroll
-                            for (int i = 0; i < LV; i++) dst[i] = eh[i];
+                            sfor<LV>([&](auto kc) {
+                                constexpr int i = decltype(kc)::value;
+                                dst[i] = Lay::keh_load(LV, i) ? eh[i] : fld<LV, Lay::eh(LV, i)>()[jt];
+                            });
                             dst[LV] = e;
                         }
                     }
