@@ -452,6 +452,9 @@ constexpr int kHrUnroll = TM_HR_UNROLL;   // edges per thread in flight (indepen
 // runs past the first sector are served one at a time by the whole warp,
 // 32 records per coalesced load, up to kHrWarpIters loads, then the gallop.
 // Must be reached by all 32 lanes (no lane may have left the loop).
+#ifndef TM_HRANK_2PHASE
+#define TM_HRANK_2PHASE 0   // measured slower: 4.71 vs 2.56 ms (profiles/r01_experiments.md)
+#endif
 #ifndef TM_HRANK_WARP_LONG
 #define TM_HRANK_WARP_LONG 0   // measured slower: 3.86 vs 2.66 ms (profiles/r01_experiments.md)
 #endif
@@ -485,7 +488,8 @@ __device__ __forceinline__ uint32_t hrank_long_warp(const uint64_t *__restrict__
 __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ rank,
                                                const uint32_t *__restrict__ vtx, const uint32_t *__restrict__ offs,
                                                const uint32_t *__restrict__ H, uint64_t m, uint32_t *__restrict__ R,
-                                               uint4 *__restrict__ W) {
+                                               uint4 *__restrict__ W, uint32_t *__restrict__ qe,
+                                               unsigned long long *__restrict__ qn) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     // warp-uniform trip count (the warp long path needs all 32 lanes)
     const uint64_t lane0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
@@ -510,7 +514,7 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
 #pragma unroll
         for (int u = 0; u < kHrUnroll; u++) {
             const uint64_t e = e0 + u * stride;
-#if !TM_HRANK_WARP_LONG
+#if !TM_HRANK_WARP_LONG && !TM_HRANK_2PHASE
             if (e >= m) break;
 #endif
             const uint32_t a = b[u] & ~3u;
@@ -523,6 +527,19 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
 #if TM_HRANK_WARP_LONG
             if (e >= m) ans = 0;   // no edge: not a long-path request
             ans = hrank_long_warp(rec, vtx, offs, e, a + 4, lim[u], ans);
+            if (e >= m) continue;
+#elif TM_HRANK_2PHASE
+            {   // long windows go to a queue for k_hrank_long (warp-aggregated append)
+                const bool lng = e < m && ans == 0xFFFFFFFFu;
+                const unsigned lm = __ballot_sync(0xffffffffu, lng);
+                if (lm) {
+                    const int lane = threadIdx.x & 31;
+                    unsigned long long base = 0;
+                    if (lane == __ffs(lm) - 1) base = atomicAdd(qn, (unsigned long long)__popc(lm));
+                    base = __shfl_sync(0xffffffffu, base, __ffs(lm) - 1);
+                    if (lng) qe[base + __popc(lm & ((1u << lane) - 1u))] = (uint32_t)e;
+                }
+            }
             if (e >= m) continue;
 #else
             if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, vtx, offs, e, a + 4, lim[u]);
@@ -591,12 +608,50 @@ tm_status set_labels(DeviceGraph &d, const int32_t *vl, const int32_t *el, bool 
     return TM_OK;
 }
 
+namespace {
+// Second phase (TM_HRANK_2PHASE): the queued edges whose window runs past the
+// first sector, one per lane, all lanes galloping (no lane waits for a
+// neighbour's long window as in the first phase).
+__global__ void __launch_bounds__(256) k_hrank_long(const uint64_t *__restrict__ rec,
+                                                    const uint32_t *__restrict__ rank,
+                                                    const uint32_t *__restrict__ vtx,
+                                                    const uint32_t *__restrict__ offs,
+                                                    const uint32_t *__restrict__ H, const uint32_t *__restrict__ qe,
+                                                    const unsigned long long *__restrict__ qn,
+                                                    uint32_t *__restrict__ R, uint4 *__restrict__ W) {
+    const unsigned long long n = *qn;
+    for (unsigned long long i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = qe[i];
+        const uint32_t ans = hrank_long(rec, vtx, offs, e, (rank[e] & ~3u) + 4, H[e]);
+        if (W) reinterpret_cast<uint32_t *>(W)[4 * (uint64_t)e + 1] = ans;
+        else R[e] = ans;
+    }
+}
+}  // namespace
+
 cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s,
                         uint4 *W) {
     if (!d.m) return cudaSuccess;
-    k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, d.rank + (size_t)var * d.m, var < 2 ? d.src : d.dst,
-                                          (var & 1) ? d.off_in : d.off_out, H, d.m, R, W);
-    return cudaGetLastError();
+    const uint32_t *rk = d.rank + (size_t)var * d.m, *vtx = var < 2 ? d.src : d.dst;
+    const uint32_t *offs = (var & 1) ? d.off_in : d.off_out;
+    if (!TM_HRANK_2PHASE) {
+        k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, rk, vtx, offs, H, d.m, R, W, nullptr, nullptr);
+        return cudaGetLastError();
+    }
+    void *q = nullptr;
+    cudaError_t err = dev_alloc(&q, d.m * sizeof(uint32_t) + 16, s);
+    if (err != cudaSuccess) return err;
+    unsigned long long *qn = (unsigned long long *)q;
+    uint32_t *qe = (uint32_t *)((char *)q + 16);
+    err = cudaMemsetAsync(qn, 0, sizeof *qn, s);
+    if (err == cudaSuccess) {
+        k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, rk, vtx, offs, H, d.m, R, W, qe, qn);
+        k_hrank_long<<<grid_for(d.m), 256, 0, s>>>(d.rec, rk, vtx, offs, H, qe, qn, R, W);
+        err = cudaGetLastError();
+    }
+    dev_free(q, s);
+    return err;
 }
 
 tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m, uint32_t n,
