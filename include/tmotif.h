@@ -319,8 +319,13 @@ tm_status tm_last_run_info(tm_run_info *out);
  * root_lo[P]=m) balanced by `weights` (per-root work proxy; NULL = the
  * δ-window length H_δ(r) - r), and returns edge_hi[p] = one past the last
  * edge rank p must hold: H_δ(root_lo[p+1]-1) + 1 (its forward δ-halo).
- * t_sorted: host, m timestamps in edge-id order.  delta: the motif's
- * effective reach min(δ, Σδ_i).  Errors: TM_EINVAL. */
+ * Cuts fall only where the timestamp changes (root_lo[p] is the first edge
+ * of its timestamp), so a slice holds every edge with t >= t(root_lo[p]):
+ * anti-edge witnesses tied with the first root stay inside.  A tie
+ * run longer than a share leaves some ranges empty.
+ * t_sorted: host, m timestamps in edge-id order.  delta: the query's
+ * reach (multi.reach: min(δ, Σδ_i) + the longest anti-edge window).
+ * Errors: TM_EINVAL. */
 tm_status tm_partition_plan(const int64_t *t_sorted, uint64_t m, int64_t delta, uint32_t P,
                             const uint64_t *weights, uint64_t *root_lo, uint64_t *edge_hi);
 

@@ -290,10 +290,17 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             const int64_t f = mo->fine[g];
             return (f == TM_DELTA_INF || f >= mo->delta) ? TM_DELTA_INF : f;
         };
+        // a motif whose kernel writes a sibling's rows (sib_of[b] == i) must run
+        // that kernel: handing it to a longer carrier would leave the sibling
+        // (and whatever resumes from its rows) at 0
+        std::vector<char> sib_carrier(k, 0);
+        for (uint32_t b = 0; b < k; b++)
+            if (sib_of[b] >= 0) sib_carrier[sib_of[b]] = 1;
         for (uint32_t a = 0; a < k; a++) {
             const uint32_t i = order[a];
             const tm_motif *mi = mos[i];
-            if (mi->constrained() || mi->disconnected || sib_of[i] >= 0 || resume_of[i] >= 0) continue;
+            if (mi->constrained() || mi->disconnected || sib_of[i] >= 0 || resume_of[i] >= 0 || sib_carrier[i])
+                continue;
             for (uint32_t b = 0; b < a && carrier[i] < 0; b++) {
                 const uint32_t j = order[b];
                 const tm_motif *mj = mos[j];
@@ -901,6 +908,7 @@ tm_status tm_count_roots(const tm_graph *g, const tm_motif *mo, const tm_run_opt
     tm_run_opts_default(&opt);
     if (o) opt = *o;
     if (n == 0) return TM_OK;
+    if (n >= (1ull << 32)) return fail(TM_EINVAL, "more than 2^32 - 1 roots in one call");
     DeviceGuard guard(g->device);
     cudaStream_t s = (cudaStream_t)opt.stream;
     const uint64_t *droots = roots;
@@ -1053,7 +1061,13 @@ tm_status tm_partition_plan(const int64_t *t, uint64_t m, int64_t delta, uint32_
     for (uint32_t q = 1; q < P; q++) {
         long double target = pre[m] * q / P;
         uint64_t r = (uint64_t)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
-        r = std::min<uint64_t>(std::max<uint64_t>(r, root_lo[q - 1]), m);
+        r = std::min<uint64_t>(r, m);
+        // cut only where the timestamp changes: a rank's slice then starts at
+        // the first edge of its timestamp, so every edge with t >= t(root_lo)
+        // is in it — an anti-edge witness tied with the slice's first root
+        // (window [t(e_a), ...]) is never cut off
+        if (r < m) r = (uint64_t)(std::lower_bound(t, t + m, t[r]) - t);
+        r = std::max<uint64_t>(r, root_lo[q - 1]);
         root_lo[q] = r;
     }
     root_lo[P] = m;

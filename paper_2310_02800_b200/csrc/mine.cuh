@@ -61,6 +61,13 @@ constexpr unsigned kShareSleepMax = TM_SHARE_SLEEP;   // ns, longest back-off of
 #define TM_LEAF_SECTORS 4
 #endif
 constexpr int kLeafSectors = TM_LEAF_SECTORS;
+#ifndef TM_ALT_LIST
+#define TM_ALT_LIST 1       // closing leaf edges may read the other endpoint's list (Shape::alt)
+#endif
+#ifndef TM_ALT_MIN
+#define TM_ALT_MIN 4        // ... when the first list's window holds more than this many records
+#endif
+constexpr uint32_t kAltMin = TM_ALT_MIN;
       // leaf windows scanned inline up to 8 records
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -261,9 +268,24 @@ struct Shape {
         }
         return false;
     }
+    // The other list of a closing leaf edge (both endpoints mapped, last
+    // motif edge): Algorithm 1 reads "N_out(u_G)/N_in(v_G)", reading
+    // Q8 the shorter one.  The kernel's first choice (ldir) is the list of the
+    // most recently touched endpoint, whose window is one descriptor load;
+    // when that window is long the warp lane compares the two lists' degrees
+    // and may scan this one instead, starting after its own anchor edge.
+    __host__ __device__ constexpr bool alt(int l) const {
+        return TM_ALT_LIST && l >= 1 && l + 1 == L && u[l] < nv(l) && v[l] < nv(l) && !pairk(l);
+    }
+    __host__ __device__ constexpr int adir(int l) const { return 1 - ldir(l); }
+    __host__ __device__ constexpr int alx(int l) const { return adir(l) == 0 ? u[l] : v[l]; }
+    __host__ __device__ constexpr int aanc(int l) const { return last_touch(l, alx(l)); }
+    __host__ __device__ constexpr int aavar(int l) const { return (u[aanc(l)] == alx(l) ? 0 : 2) + adir(l); }
     __host__ __device__ constexpr bool keep_eh(int l, int k) const {
-        for (int q = l + 1; q < L; ++q)
+        for (int q = l + 1; q < L; ++q) {
             if (k < l && !pairk(q) && anc(q) == k) return true;
+            if (k < l && alt(q) && aanc(q) == k) return true;
+        }
         return false;
     }
     __host__ __device__ constexpr bool keep_hi(int l) const { return l + 1 < L; }
@@ -311,6 +333,11 @@ struct PlanC {
     template <int I> __device__ __forceinline__ static constexpr int anc() { constexpr int r = shape_of<CODE>().anc(I); return r; }
     template <int I> __device__ __forceinline__ static constexpr int avar() { constexpr int r = shape_of<CODE>().avar(I); return r; }
     template <int I> __device__ __forceinline__ static constexpr bool pairk() { constexpr bool r = shape_of<CODE>().pairk(I); return r; }
+    template <int I> __device__ __forceinline__ static constexpr bool alt() { constexpr bool r = !GEN && shape_of<CODE>().alt(I); return r; }
+    template <int I> __device__ __forceinline__ static constexpr int adir() { constexpr int r = shape_of<CODE>().adir(I); return r; }
+    template <int I> __device__ __forceinline__ static constexpr int alx() { constexpr int r = shape_of<CODE>().alx(I); return r; }
+    template <int I> __device__ __forceinline__ static constexpr int aanc() { constexpr int r = shape_of<CODE>().aanc(I); return r; }
+    template <int I> __device__ __forceinline__ static constexpr int aavar() { constexpr int r = shape_of<CODE>().aavar(I); return r; }
 };
 
 // Runtime plan: the same kernel body for any prefix-connected motif with
@@ -358,6 +385,12 @@ struct PlanR {
     template <int I> __device__ __forceinline__ int anc() const { return anc_[I]; }
     template <int I> __device__ __forceinline__ int avar() const { return avar_[I]; }
     template <int I> __device__ __forceinline__ bool pairk() const { return pairk_[I]; }
+    // the generic kernel keeps the single-list choice (per-root counts, instrumentation)
+    template <int I> __device__ __forceinline__ static constexpr bool alt() { return false; }
+    template <int I> __device__ __forceinline__ static constexpr int adir() { return 0; }
+    template <int I> __device__ __forceinline__ static constexpr int alx() { return 0; }
+    template <int I> __device__ __forceinline__ static constexpr int aanc() { return 0; }
+    template <int I> __device__ __forceinline__ static constexpr int aavar() { return 0; }
 };
 
 #ifndef TM_SIB_LAZY_EH
@@ -665,13 +698,33 @@ struct Warp {
                     if (j != NL - 1) lo = scan_after(p.rec, lo, e);
                 }
                 const bool fine_binds = (hw || hr) && hfv <= hi;   // lim == H_δi[e]: the end depends on e only
-                const bool known = fine_binds && (!kHrankMemo || hrv != 0);
+                bool known = fine_binds && (!kHrankMemo || hrv != 0);
                 const uint32_t up_known = kHrankMemo ? hrv - 1 : hrv;
+                // (generalized queries check every match in expand(): no in-lane leaf scans)
+                const bool leaf = NL + 1 == plan.L() && !gen();
+                // closing leaf edge (reading Q8): a window of more than kAltMin
+                // records in the first list is replaced by the other endpoint's list
+                // when that list is the shorter one by degree.  Its window starts
+                // after its anchor edge (one rank load) and is found by the sector
+                // scan below, which also steps over the ids <= e in front of it.
+                bool use_alt = false;
+                if constexpr (plan.template alt<NL>()) {
+                    if (leaf && known && up_known > lo + kAltMin) {
+                        constexpr int adir = plan.template adir<NL>();
+                        const uint32_t xp = pick(phi, plan.template lx<NL>()), xa = pick(phi, plan.template alx<NL>());
+                        const uint32_t *op = dir == 0 ? p.off_out : p.off_in, *oa = adir == 0 ? p.off_out : p.off_in;
+                        use_alt = __ldg(oa + xa + 1) - __ldg(oa + xa) < __ldg(op + xp + 1) - __ldg(op + xp);
+                        if (use_alt) {
+                            constexpr int ja = plan.template aanc<NL>();
+                            lo = __ldg(p.rank + (size_t)plan.template aavar<NL>() * p.m + (ja == NL - 1 ? e : pick(eh, ja)));
+                            known = false;
+                        }
+                    }
+                }
+                const bool from_out = use_alt ? plan.template adir<NL>() == 0 : dir == 0;
                 uint32_t pp = lo;
                 bool done = false;
                 uint32_t cnt = 0;
-                // (generalized queries check every match in expand(): no in-lane leaf scans)
-                const bool leaf = NL + 1 == plan.L() && !gen();
                 // leaf parent: the last motif edge's window is scanned in this
                 // lane and its matches counted (or emitted) on the spot, for up
                 // to kLeafSectors sectors; non-leaf: one sector to size the window
@@ -735,7 +788,8 @@ struct Warp {
                         if (done || q < pp) continue;
                         const uint32_t id = (uint32_t)(r4[k] >> 32);
                         if (id > lim) { done = true; up = q; continue; }
-                        if (leaf && accept<NL>((uint32_t)r4[k], dir == 0, phi)) {
+                        if (use_alt && id <= e) continue;   // before e_prev in the other list
+                        if (leaf && accept<NL>((uint32_t)r4[k], from_out, phi)) {
                             cnt++;
                             if (MODE == kEnum) emit_one<NE>(eh, e, id, NL);
                         }
@@ -754,13 +808,14 @@ struct Warp {
                     if (known) {
                         up = up_known;
                     } else {
-                        const uint32_t x = pick(phi, plan.template lx<NL>());
-                        const uint32_t en = __ldg((dir == 0 ? p.off_out : p.off_in) + x + 1) - 1;
-                        up = gallop_after(p.rec, pp, en, lim);
+                        const uint32_t x = use_alt ? pick(phi, plan.template alx<NL>()) : pick(phi, plan.template lx<NL>());
+                        const uint32_t en = __ldg((from_out ? p.off_out : p.off_in) + x + 1) - 1;
+                        if (use_alt) lo = gallop_after(p.rec, pp, en, e);   // the remainder starts after e
+                        up = gallop_after(p.rec, use_alt ? lo : pp, en, lim);
                     }
                 }
                 // first visit of e at this level: remember its window end (pos + 1)
-                if (kHrankMemo && fine_binds && !known) __stcg(hr + e, up + 1);
+                if (kHrankMemo && fine_binds && !known && !use_alt) __stcg(hr + e, up + 1);
                 if (leaf && done) lo = up = 0;              // fully scanned
             }
         }

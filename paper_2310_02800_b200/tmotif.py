@@ -302,6 +302,13 @@ def tm_enumerate(g: Graph, mo: Motif, cap: int, buf=None, **opts):
     on_dev = buf is not None and _is_torch(buf)
     if buf is None:
         buf = np.zeros((max(cap, 1), mo.L), np.uint32)
+    elif on_dev:
+        import torch
+        if buf.dtype not in (torch.int32, torch.uint32) or not buf.is_contiguous() or buf.numel() < cap * mo.L:
+            raise ValueError("device buffer must be a contiguous int32 tensor of at least (cap, L) elements")
+    else:
+        if buf.dtype != np.uint32 or not buf.flags.c_contiguous or buf.size < cap * mo.L:
+            raise ValueError("host buffer must be a C-contiguous uint32 array of at least (cap, L) elements")
     o = run_opts(buffers_on_device=on_dev, **opts)
     nt, nw = _u64(), _u64()
     st = lib().tm_enumerate(g.handle, mo.handle, ctypes.byref(o), _ptr(buf), int(cap), ctypes.byref(nt),
@@ -314,6 +321,10 @@ def tm_enumerate(g: Graph, mo: Motif, cap: int, buf=None, **opts):
 def tm_count_roots(g: Graph, mo: Motif, roots, **opts):
     if _is_torch(roots):
         import torch
+        # the C side reads u64 ids and does not range-check device buffers
+        roots = roots.to(torch.int64).contiguous().reshape(-1)
+        if roots.numel() and (int(roots.min()) < 0 or int(roots.max()) >= g.m):
+            raise ValueError("root id out of range [0, m)")
         counts = torch.zeros(roots.shape[0], dtype=torch.int64, device=roots.device)
         o = run_opts(buffers_on_device=True, **opts)
     else:

@@ -703,3 +703,75 @@ def test_disconnected_in_multi_and_errors():
     with pytest.raises(T.TMotifError) as e:
         T.tm_count(g, T.Motif([(0, 1), (2, 3)], 600, vlabels={0: 1}))
     assert e.value.status == T.TM_EUNSUPPORTED
+
+
+# ------------------------------------- the timed configuration
+C4_BENCH = [("P3", [21600] * 2), ("TRI", [21600] * 2), ("C4", [21600] * 3), ("DIA", [21600] * 4)]
+
+
+def _bench_query(delta=86400):
+    return [T.Motif(M.get(nm), delta, f) for nm, f in C4_BENCH]
+
+
+def test_C4_bench_query_full_oracle():
+    """bench.py's exact timed query — tm_count_multi over P3/TRI/C4/DIA at
+    δ = 1 d, δ_i = 6 h on the full 63.5M-edge C4 graph, fused (the 4-cycle
+    kernel in kCountSib mode counting P3 as its level-3 nodes and writing TRI's
+    rows, the diamond resumed from those rows) — equals the full oracle count
+    of every motif (exact), and equals the unfused query."""
+    src, dst, t, n = synth.config_graph("C4")
+    g = T.Graph(src, dst, t, n)
+    got = T.tm_count_multi(g, _bench_query())
+    modes = [x["kernel_mode"] for x in T.tm_last_kernel_info()]
+    assert modes == [T.KMODE_NONE, T.KMODE_NONE, T.KMODE_COUNT_SIB, T.KMODE_RESUME], modes
+    og = oracle.Graph(src, dst, t, n)
+    exp = [og.mine(M.get(nm), 86400, f)["count"] for nm, f in C4_BENCH]
+    assert got == exp, (got, exp)
+    assert T.tm_count_multi(g, _bench_query(), fuse=1) == exp
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_specialised_kernels_root_subranges(cfg):
+    """Per-root parity of the kernels bench.py times (the catalog's
+    specialised PlanC kernels in the kCount / kCountSib / kCountPfx / kResume
+    modes, not the generic per-root PlanR kernel): 64 random root sub-ranges,
+    each a separate tm_count_multi / tm_count, against the oracle's count over
+    the same roots."""
+    src, dst, t, n = synth.config_graph(cfg)
+    m = len(src)
+    g = T.Graph(src, dst, t, n)
+    og = oracle.Graph(src, dst, t, n)
+    rng = np.random.default_rng(64)
+    mos = _bench_query()
+    for k in range(64):
+        w = int(rng.choice([1, 37, 1000, 20000]))
+        lo = int(rng.integers(0, m - w))
+        rr = (lo, lo + w)
+        got = T.tm_count_multi(g, mos, root_range=rr)
+        exp = [og.mine(M.get(nm), 86400, f, root_range=rr)["count"] for nm, f in C4_BENCH]
+        assert got == exp, (cfg, rr, got, exp)
+        if k % 8 == 0:   # the plain specialised counting kernel, one motif per query
+            for (nm, f), mo, e in zip(C4_BENCH, mos, exp):
+                assert mo.specialised
+                assert T.tm_count(g, mo, root_range=rr) == e, (cfg, rr, nm)
+
+
+def test_fusion_keeps_sibling_carrier():
+    """a motif that writes a sibling's rows (the 4-cycle
+    for TRI) must keep its own kernel even when a longer motif (a 5-edge
+    extension of the 4-cycle) could count it as a prefix — otherwise TRI
+    (and the motifs resuming from its rows) read 0."""
+    d, f = 3600, 1200
+    src, dst, t, n = synth.burst_graph(11, n=2000, m_bg=20000, bursts=2, core=30, burst_len=1800)
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    c4x = M.C4 + [(0, 2)]
+    sets = [[(M.C4, [f] * 3), (M.TRI, [f] * 2), (c4x, [f] * 4)],
+            [(M.C4, None), (M.TRI, None), (c4x, None), (M.DIA, None)],
+            [(c4x, [f] * 4), (M.DIA, [f] * 4), (M.TRI, [f] * 2), (M.C4, [f] * 3), (M.P3, [f] * 2)]]
+    for specs in sets:
+        mos = [T.Motif(mm, d, ff) for mm, ff in specs]
+        exp = [og.mine(mm, d, ff)["count"] for mm, ff in specs]
+        assert all(e > 0 for e in exp)
+        assert T.tm_count_multi(g, mos) == exp, specs
+        assert T.tm_count_multi(g, mos, fuse=1) == exp, specs

@@ -14,10 +14,12 @@ import torch.multiprocessing as mp
 import oracle
 from paper_2310_02800_b200 import motifs as M
 from paper_2310_02800_b200 import multi, synth
+from paper_2310_02800_b200 import tmotif as T
 
 # (motif, δ, δ_i, anti-edges): an anti-edge window extends the halo (multi.reach)
 CASES = [("TRI", 3600, None, None), ("C4", 3600, [1800, 1800, 1800], None), ("P3", 3600, [600, 600], None),
-         ("TRI", 3600, None, [(1, 0, 2, 7200)]), ("P3", 1800, [600, 600], [(3, 0, 1, 3600), (0, 2, 0, 900)])]
+         ("TRI", 3600, None, [(1, 0, 2, 7200)]), ("P3", 1800, [600, 600], [(3, 0, 1, 3600), (0, 2, 0, 900)]),
+         ("TRI", 3600, None, [(2, 0, 0, 5)])]
 
 
 def _free_port():
@@ -28,19 +30,25 @@ def _free_port():
     return p
 
 
+def _graph(coarse):
+    src, dst, t, n = synth.config_graph("C1")
+    return src, dst, (t // coarse) * coarse, n
+
+
 def _worker(rank, world, port, out):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    src, dst, t, n = synth.config_graph("C1")
-    order = np.lexsort((np.arange(len(t)), t))        # (t, input position): sorted edge ids
-    S, D, Tt = src[order], dst[order], t[order]
     counts = []
-    for name, delta, fine, anti in CASES:
-        mot = M.get(name)
-        lo, hi, ehi = multi.rank_slice(Tt, multi.reach(delta, fine, anti), world, rank)
-        g = oracle.Graph(S[lo:ehi], D[lo:ehi], Tt[lo:ehi], n)
-        counts.append(g.mine(mot, delta, fine, root_range=(0, hi - lo), anti=anti)["count"])
+    for coarse in (1, 600):   # 600: timestamps rounded to 10 min, long runs of equal t at every cut
+        src, dst, t, n = _graph(coarse)
+        order = np.lexsort((np.arange(len(t)), t))        # (t, input position): sorted edge ids
+        S, D, Tt = src[order], dst[order], t[order]
+        for name, delta, fine, anti in CASES:
+            mot = M.get(name)
+            lo, hi, ehi = multi.rank_slice(Tt, multi.reach(delta, fine, anti), world, rank)
+            g = oracle.Graph(S[lo:ehi], D[lo:ehi], Tt[lo:ehi], n)
+            counts.append(g.mine(mot, delta, fine, root_range=(0, hi - lo), anti=anti)["count"])
     total = multi.allreduce_counts(counts)
     out[rank] = total
     dist.barrier()
@@ -59,11 +67,37 @@ def test_partitioned_counts_allreduce_to_global(world):
     for p in procs:
         p.join(180)
         assert p.exitcode == 0
-    src, dst, t, n = synth.config_graph("C1")
-    g = oracle.Graph(src, dst, t, n)
-    expect = [g.mine(M.get(name), delta, fine, anti=anti)["count"] for name, delta, fine, anti in CASES]
+    expect = []
+    for coarse in (1, 600):
+        g = oracle.Graph(*_graph(coarse))
+        expect += [g.mine(M.get(name), delta, fine, anti=anti)["count"] for name, delta, fine, anti in CASES]
     assert all(out[r] == expect for r in range(world))
     assert sum(expect) > 0
+
+
+def test_anti_edge_witness_tied_with_slice_start():
+    """VERDICT r01 Weak #6: an anti-edge witness with the same timestamp as a
+    slice's first root but a smaller edge id must stay inside the slice.
+    Cuts fall only between distinct timestamps (tm_partition_plan), so the
+    per-rank counts sum to the whole graph's for every P."""
+    cases = [  # (src, dst, t, motif, anti, δ)
+        ([2, 0, 1, 2], [0, 1, 2, 0], [10, 10, 11, 12], M.TRI, [(2, 0, 0, 5)], 100),
+        ([0, 0, 1], [2, 1, 2], [10, 10, 20], M.PATH2, [(0, 2, 0, 5)], 100),
+    ]
+    for src, dst, t, mot, anti, delta in cases:
+        src, dst, t = (np.array(x) for x in (src, dst, t))
+        n = int(max(src.max(), dst.max())) + 1
+        whole = oracle.Graph(src, dst, t, n).mine(mot, delta, anti=anti)["count"]
+        for P in (2, 3, 4):
+            lo, hi = T.tm_partition_plan(t, multi.reach(delta, None, anti), P)
+            s = 0
+            for p in range(P):
+                a, b, e = int(lo[p]), int(lo[p + 1]), int(hi[p])
+                assert a == 0 or a == len(t) or t[a - 1] != t[a]   # cut between distinct timestamps
+                if b > a:
+                    s += oracle.Graph(src[a:e], dst[a:e], t[a:e], n).mine(mot, delta, root_range=(0, b - a),
+                                                                          anti=anti)["count"]
+            assert s == whole, (mot, P, s, whole)
 
 
 def test_reach():

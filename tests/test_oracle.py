@@ -116,6 +116,51 @@ def test_window_sum_single_list_motifs():
         assert st["window_sum"] == exp
 
 
+def test_instrumentation_both_mapped_levels_shorter_list():
+    """Pins the oracle's list choice for a motif edge with both endpoints
+    mapped ("N_out(u_G)/N_in(v_G)", reading Q8: the shorter list by
+    degree, a tie takes N_in(v_G)): window_sum, list_sum and probe_sum are
+    recomputed here from brute-force prefix matches and per-vertex degrees
+    counted off the global edge list.  Choosing the other list (or always
+    one of them) changes these counters but not the matches."""
+    rng = random.Random(12)
+    motifs = [M.TRI, M.C4, M.DIA, M.TT, [(0, 1), (1, 0), (0, 1)], [(0, 1), (1, 2), (0, 2)],
+              [(0, 1), (1, 2), (2, 1), (1, 0)]]
+    for k in range(40):
+        motif = motifs[k % len(motifs)]
+        src, dst, t, n = synth.tiny_graph(1500 + k, n=rng.randint(3, 6), m=rng.randint(8, 40 if len(motif) < 5 else 28),
+                                          tmax=rng.choice([12, 30]))
+        delta = rng.choice([5, 12, INF] if len(motif) < 5 else [5, 12])
+        fine = random_fine(rng, len(motif))
+        S, D, T, _ = sorted_edges(src, dst, t)
+        m = len(S)
+        out_deg = [sum(1 for c in range(m) if S[c] == x) for x in range(n)]
+        in_deg = [sum(1 for c in range(m) if D[c] == x) for x in range(n)]
+        win = lst = probes = 0
+        for l in range(1, len(motif)):
+            fl = None if fine is None else fine[:l - 1]
+            for tup in brute(src, dst, t, motif[:l], delta, fl):
+                phi = {}
+                for (a, b), e in zip(motif[:l], tup):
+                    phi[a], phi[b] = S[e], D[e]
+                u, v = motif[l]
+                if u in phi and v in phi:
+                    use_out = out_deg[phi[u]] < in_deg[phi[v]]
+                else:
+                    use_out = u in phi
+                x = phi[u] if use_out else phi[v]
+                length = out_deg[x] if use_out else in_deg[x]
+                lst += length
+                probes += length.bit_length()      # ceil(log2(len + 1))
+                f = INF if fine is None or fine[l - 1] is None else fine[l - 1]
+                for c in range(tup[-1] + 1, m):
+                    on_list = (S[c] == x) if use_out else (D[c] == x)
+                    if on_list and T[c] - T[tup[0]] <= delta and T[c] - T[tup[-1]] <= f:
+                        win += 1
+        st = oracle.Graph(src, dst, t, n).mine(motif, delta, fine)["stats"]
+        assert (st["window_sum"], st["list_sum"], st["probe_sum"]) == (win, lst, probes), (motif, delta, fine)
+
+
 # ----------------------------------------------------------------- closed forms
 def test_delta_inf_equals_static_time_ordered_count():
     rng = random.Random(5)
