@@ -62,7 +62,7 @@ constexpr unsigned kShareSleepMax = TM_SHARE_SLEEP;   // ns, longest back-off of
 #endif
 constexpr int kLeafSectors = TM_LEAF_SECTORS;
 #ifndef TM_ALT_LIST
-#define TM_ALT_LIST 1       // closing leaf edges may read the other endpoint's list (Shape::alt)
+#define TM_ALT_LIST 0       // (measured slower: C4 step 13.74 -> 15.82 ms) closing leaf edges may read the other endpoint's list (Shape::alt)
 #endif
 #ifndef TM_ALT_MIN
 #define TM_ALT_MIN 4        // ... when the first list's window holds more than this many records
@@ -708,14 +708,14 @@ struct Warp {
                 // after its anchor edge (one rank load) and is found by the sector
                 // scan below, which also steps over the ids <= e in front of it.
                 bool use_alt = false;
-                if constexpr (plan.template alt<NL>()) {
+                if constexpr (Plan::template alt<NL>()) {
                     if (leaf && known && up_known > lo + kAltMin) {
-                        constexpr int adir = plan.template adir<NL>();
+                        constexpr int adir = Plan::template adir<NL>();
                         const uint32_t xp = pick(phi, plan.template lx<NL>()), xa = pick(phi, plan.template alx<NL>());
                         const uint32_t *op = dir == 0 ? p.off_out : p.off_in, *oa = adir == 0 ? p.off_out : p.off_in;
                         use_alt = __ldg(oa + xa + 1) - __ldg(oa + xa) < __ldg(op + xp + 1) - __ldg(op + xp);
                         if (use_alt) {
-                            constexpr int ja = plan.template aanc<NL>();
+                            constexpr int ja = Plan::template aanc<NL>();
                             lo = __ldg(p.rank + (size_t)plan.template aavar<NL>() * p.m + (ja == NL - 1 ? e : pick(eh, ja)));
                             known = false;
                         }
