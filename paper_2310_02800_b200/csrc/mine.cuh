@@ -61,13 +61,9 @@ constexpr unsigned kShareSleepMax = TM_SHARE_SLEEP;   // ns, longest back-off of
 #define TM_LEAF_SECTORS 4
 #endif
 constexpr int kLeafSectors = TM_LEAF_SECTORS;
-#ifndef TM_ALT_LIST
-#define TM_ALT_LIST 0       // (measured slower: C4 step 13.74 -> 15.82 ms) closing leaf edges may read the other endpoint's list (Shape::alt)
+#ifndef TM_LOOKAHEAD
+#define TM_LOOKAHEAD 1      // closing look-ahead bound from the root (Shape::look)
 #endif
-#ifndef TM_ALT_MIN
-#define TM_ALT_MIN 4        // ... when the first list's window holds more than this many records
-#endif
-constexpr uint32_t kAltMin = TM_ALT_MIN;
       // leaf windows scanned inline up to 8 records
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -268,24 +264,29 @@ struct Shape {
         }
         return false;
     }
-    // The other list of a closing leaf edge (both endpoints mapped, last
-    // motif edge): Algorithm 1 reads "N_out(u_G)/N_in(v_G)", reading
-    // Q8 the shorter one.  The kernel's first choice (ldir) is the list of the
-    // most recently touched endpoint, whose window is one descriptor load;
-    // when that window is long the warp lane compares the two lists' degrees
-    // and may scan this one instead, starting after its own anchor edge.
-    __host__ __device__ constexpr bool alt(int l) const {
-        return TM_ALT_LIST && l >= 1 && l + 1 == L && u[l] < nv(l) && v[l] < nv(l) && !pairk(l);
+    // Closing look-ahead.  The last motif edge with both endpoints mapped is
+    // an edge between two bound vertices, so it lies in BOTH of their lists
+    // (Algorithm 1 may read either, "N_out(u_G)/N_in(v_G)").  The
+    // kernel scans the list of the most recently touched endpoint (ldir);
+    // when the other endpoint y is an endpoint of the root edge (motif vertex
+    // 0 or 1), every match's last edge is also a record of y's other-direction
+    // list with id in (e_1, H_δ(e_1)].  The root reads that list's window once
+    // (one rank load, one sector): LI = the id of its last record, 0 when it
+    // is empty, hi when the window runs past the sector (no bound).  Every
+    // closing window is then (e_{L-1}, min(lim, LI)]: empty without a single
+    // load when e_{L-1} >= LI.  The search tree is unchanged (the closing
+    // edge is a leaf), so the counts, the matches and every level's nodes are
+    // Algorithm 1's; only the leaf scans shrink.
+    __host__ __device__ constexpr int lkdir() const { return 1 - ldir(L - 1); }
+    __host__ __device__ constexpr int lky() const { return lkdir() == 0 ? u[L - 1] : v[L - 1]; }
+    __host__ __device__ constexpr bool look() const {
+        return TM_LOOKAHEAD && L >= 3 && u[L - 1] < nv(L - 1) && v[L - 1] < nv(L - 1) && !pairk(L - 1) && lky() <= 1;
     }
-    __host__ __device__ constexpr int adir(int l) const { return 1 - ldir(l); }
-    __host__ __device__ constexpr int alx(int l) const { return adir(l) == 0 ? u[l] : v[l]; }
-    __host__ __device__ constexpr int aanc(int l) const { return last_touch(l, alx(l)); }
-    __host__ __device__ constexpr int aavar(int l) const { return (u[aanc(l)] == alx(l) ? 0 : 2) + adir(l); }
+    // rank variant of the root edge in y's list: 2 * (endpoint of e_1) + direction
+    __host__ __device__ constexpr int lkvar() const { return (lky() == 0 ? 0 : 2) + lkdir(); }
     __host__ __device__ constexpr bool keep_eh(int l, int k) const {
-        for (int q = l + 1; q < L; ++q) {
+        for (int q = l + 1; q < L; ++q)
             if (k < l && !pairk(q) && anc(q) == k) return true;
-            if (k < l && alt(q) && aanc(q) == k) return true;
-        }
         return false;
     }
     __host__ __device__ constexpr bool keep_hi(int l) const { return l + 1 < L; }
@@ -333,11 +334,8 @@ struct PlanC {
     template <int I> __device__ __forceinline__ static constexpr int anc() { constexpr int r = shape_of<CODE>().anc(I); return r; }
     template <int I> __device__ __forceinline__ static constexpr int avar() { constexpr int r = shape_of<CODE>().avar(I); return r; }
     template <int I> __device__ __forceinline__ static constexpr bool pairk() { constexpr bool r = shape_of<CODE>().pairk(I); return r; }
-    template <int I> __device__ __forceinline__ static constexpr bool alt() { constexpr bool r = !GEN && shape_of<CODE>().alt(I); return r; }
-    template <int I> __device__ __forceinline__ static constexpr int adir() { constexpr int r = shape_of<CODE>().adir(I); return r; }
-    template <int I> __device__ __forceinline__ static constexpr int alx() { constexpr int r = shape_of<CODE>().alx(I); return r; }
-    template <int I> __device__ __forceinline__ static constexpr int aanc() { constexpr int r = shape_of<CODE>().aanc(I); return r; }
-    template <int I> __device__ __forceinline__ static constexpr int aavar() { constexpr int r = shape_of<CODE>().aavar(I); return r; }
+    __host__ __device__ static constexpr bool look() { return !GEN && shape_of<CODE>().look(); }
+    __host__ __device__ static constexpr int lkvar() { return shape_of<CODE>().lkvar(); }
 };
 
 // Runtime plan: the same kernel body for any prefix-connected motif with
@@ -385,12 +383,9 @@ struct PlanR {
     template <int I> __device__ __forceinline__ int anc() const { return anc_[I]; }
     template <int I> __device__ __forceinline__ int avar() const { return avar_[I]; }
     template <int I> __device__ __forceinline__ bool pairk() const { return pairk_[I]; }
-    // the generic kernel keeps the single-list choice (per-root counts, instrumentation)
-    template <int I> __device__ __forceinline__ static constexpr bool alt() { return false; }
-    template <int I> __device__ __forceinline__ static constexpr int adir() { return 0; }
-    template <int I> __device__ __forceinline__ static constexpr int alx() { return 0; }
-    template <int I> __device__ __forceinline__ static constexpr int aanc() { return 0; }
-    template <int I> __device__ __forceinline__ static constexpr int aavar() { return 0; }
+    // no closing look-ahead in the generic kernel (per-root counts, instrumentation)
+    __host__ __device__ static constexpr bool look() { return false; }
+    __host__ __device__ static constexpr int lkvar() { return 0; }
 };
 
 #ifndef TM_SIB_LAZY_EH
@@ -416,14 +411,18 @@ struct Layout {
         return keh(l, k) && !(TM_SIB_LAZY_EH && MODE == kCountSib && l == kSibLevel && k < l && !Plan::keep_eh(l, k));
     }
     __host__ __device__ static constexpr bool khi(int l) { return MODE == kStats || Plan::keep_hi(l); }
+    // the closing look-ahead bound (Shape::look) of the root, carried to level L-2
+    __host__ __device__ static constexpr bool look() { return MODE != kStats && Plan::look(); }
+    __host__ __device__ static constexpr bool kli(int l) { return look() && l >= 1 && l + 3 <= Plan::kL; }
     __host__ __device__ static constexpr int phi(int l, int k) {
         int f = 2;
         for (int i = 0; i < k; i++) f += kphi(l, i) ? 1 : 0;
         return f;
     }
     __host__ __device__ static constexpr int hi(int l) { return phi(l, Plan::nslots(l)); }
+    __host__ __device__ static constexpr int li(int l) { return hi(l) + (khi(l) ? 1 : 0); }
     __host__ __device__ static constexpr int eh(int l, int k) {
-        int f = hi(l) + (khi(l) ? 1 : 0);
+        int f = li(l) + (kli(l) ? 1 : 0);
         for (int i = 0; i < k; i++) f += keh(l, i) ? 1 : 0;
         return f;
     }
@@ -605,9 +604,11 @@ struct Warp {
     // matched edges, last edge e, bound vertices phi.  Searches the candidate
     // window of motif edge NL (GetCandidateEdgeList) and pushes the
     // task if the window is non-empty.
+    // li: the root's closing look-ahead bound (Shape::look; ~0u = none).
     template <int NL, int NS, int NE>
     __device__ __forceinline__ void push(bool ok, uint32_t e, uint32_t hi, const uint32_t (&phi)[NS],
-                                         const uint32_t (&eh)[NE], uint32_t rslot) {
+                                         const uint32_t (&eh)[NE], uint32_t rslot, uint32_t li = ~0u) {
+        using Lay = Layout<Plan, MODE>;
         uint32_t lo = 0, up = 0;
         if ((MODE == kCountPfx || MODE == kCountSib) && (p.prefix_mask >> NL) & 1u) {   // matches of the NL-edge prefix
             if (NL == p.prefix_lv0) {
@@ -617,7 +618,11 @@ struct Warp {
                 if (lane == 0 && c) atomicAdd(p.scratch + kPrefixBase + NL, (unsigned long long)c);
             }
         }
-        if (ok) {
+        // closing edge under the look-ahead: hi is min(H_δ(e_1), LI); a match's
+        // last edge would have to lie in (e, hi], none does when e >= hi
+        bool live = ok;
+        if constexpr (Lay::look() && NL + 1 == Plan::kL) live = ok && e < hi;
+        if (live) {
             const uint32_t *hf = p.Hf[NL - 1];
             uint32_t lim = hi;   // min(t_root + δ, t_prev + δ_i) as an id; H_δi read when needed
             uint32_t hfv = ~0u;
@@ -698,30 +703,10 @@ struct Warp {
                     if (j != NL - 1) lo = scan_after(p.rec, lo, e);
                 }
                 const bool fine_binds = (hw || hr) && hfv <= hi;   // lim == H_δi[e]: the end depends on e only
-                bool known = fine_binds && (!kHrankMemo || hrv != 0);
+                const bool known = fine_binds && (!kHrankMemo || hrv != 0);
                 const uint32_t up_known = kHrankMemo ? hrv - 1 : hrv;
                 // (generalized queries check every match in expand(): no in-lane leaf scans)
                 const bool leaf = NL + 1 == plan.L() && !gen();
-                // closing leaf edge (reading Q8): a window of more than kAltMin
-                // records in the first list is replaced by the other endpoint's list
-                // when that list is the shorter one by degree.  Its window starts
-                // after its anchor edge (one rank load) and is found by the sector
-                // scan below, which also steps over the ids <= e in front of it.
-                bool use_alt = false;
-                if constexpr (Plan::template alt<NL>()) {
-                    if (leaf && known && up_known > lo + kAltMin) {
-                        constexpr int adir = Plan::template adir<NL>();
-                        const uint32_t xp = pick(phi, plan.template lx<NL>()), xa = pick(phi, plan.template alx<NL>());
-                        const uint32_t *op = dir == 0 ? p.off_out : p.off_in, *oa = adir == 0 ? p.off_out : p.off_in;
-                        use_alt = __ldg(oa + xa + 1) - __ldg(oa + xa) < __ldg(op + xp + 1) - __ldg(op + xp);
-                        if (use_alt) {
-                            constexpr int ja = Plan::template aanc<NL>();
-                            lo = __ldg(p.rank + (size_t)plan.template aavar<NL>() * p.m + (ja == NL - 1 ? e : pick(eh, ja)));
-                            known = false;
-                        }
-                    }
-                }
-                const bool from_out = use_alt ? plan.template adir<NL>() == 0 : dir == 0;
                 uint32_t pp = lo;
                 bool done = false;
                 uint32_t cnt = 0;
@@ -788,8 +773,7 @@ struct Warp {
                         if (done || q < pp) continue;
                         const uint32_t id = (uint32_t)(r4[k] >> 32);
                         if (id > lim) { done = true; up = q; continue; }
-                        if (use_alt && id <= e) continue;   // before e_prev in the other list
-                        if (leaf && accept<NL>((uint32_t)r4[k], from_out, phi)) {
+                        if (leaf && accept<NL>((uint32_t)r4[k], dir == 0, phi)) {
                             cnt++;
                             if (MODE == kEnum) emit_one<NE>(eh, e, id, NL);
                         }
@@ -808,14 +792,13 @@ struct Warp {
                     if (known) {
                         up = up_known;
                     } else {
-                        const uint32_t x = use_alt ? pick(phi, plan.template alx<NL>()) : pick(phi, plan.template lx<NL>());
-                        const uint32_t en = __ldg((from_out ? p.off_out : p.off_in) + x + 1) - 1;
-                        if (use_alt) lo = gallop_after(p.rec, pp, en, e);   // the remainder starts after e
-                        up = gallop_after(p.rec, use_alt ? lo : pp, en, lim);
+                        const uint32_t x = pick(phi, plan.template lx<NL>());
+                        const uint32_t en = __ldg((dir == 0 ? p.off_out : p.off_in) + x + 1) - 1;
+                        up = gallop_after(p.rec, pp, en, lim);
                     }
                 }
                 // first visit of e at this level: remember its window end (pos + 1)
-                if (kHrankMemo && fine_binds && !known && !use_alt) __stcg(hr + e, up + 1);
+                if (kHrankMemo && fine_binds && !known) __stcg(hr + e, up + 1);
                 if (leaf && done) lo = up = 0;              // fully scanned
             }
         }
@@ -824,7 +807,6 @@ struct Warp {
         if (!mask) return;
         if (keep) {
             const uint32_t slot = ntask[NL] + __popc(mask & lanemask_lt());
-            using Lay = Layout<Plan, MODE>;
             fld<NL, 0>()[slot] = lo;
             fld<NL, 1>()[slot] = up;
             constexpr int S = Plan::nslots(NL);
@@ -832,7 +814,11 @@ struct Warp {
                 constexpr int k = decltype(kc)::value;
                 if constexpr (Lay::kphi(NL, k)) fld<NL, Lay::phi(NL, k)>()[slot] = phi[k < NS ? k : 0];
             });
-            if constexpr (Lay::khi(NL)) fld<NL, Lay::hi(NL)>()[slot] = hi;
+            if constexpr (Lay::khi(NL)) {   // level L-2: hi only bounds the closing window
+                if constexpr (Lay::look() && NL + 2 == Plan::kL) fld<NL, Lay::hi(NL)>()[slot] = min(hi, li);
+                else fld<NL, Lay::hi(NL)>()[slot] = hi;
+            }
+            if constexpr (Lay::kli(NL)) fld<NL, Lay::li(NL)>()[slot] = li;
             sfor<NL>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
                 if constexpr (Lay::keh(NL, k)) fld<NL, Lay::eh(NL, k)>()[slot] = (k < NL - 1) ? eh[k < NE ? k : 0] : e;
@@ -875,6 +861,32 @@ struct Warp {
             for (int i = 0; i < NL; i++) eh[i] = 0u;
         }
         push<NL>(ok, eh[NL - 1], hi, phi, eh, slot);
+    }
+
+    // The closing look-ahead bound of root r (Shape::look): the id of the
+    // last record of y's list in (r, hi], 0 if there is none, hi if that
+    // window runs past the aligned sector holding its start (no gallop: an
+    // upper bound is as correct, only less selective).
+    __device__ __forceinline__ uint32_t look_ahead(uint32_t r, uint32_t hi) const {
+        const uint32_t b = __ldg(p.rank + (size_t)Plan::lkvar() * p.m + r);   // first record after r
+        const uint32_t a4 = b & ~3u;
+        const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(p.rec + a4);
+        const ulonglong2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
+        const uint32_t id[4] = {(uint32_t)(x0.x >> 32), (uint32_t)(x0.y >> 32), (uint32_t)(x1.x >> 32),
+                                (uint32_t)(x1.y >> 32)};
+        // the first record past hi: ids ascend up to the list's sentinel (id
+        // 0xFFFFFFFF), so it is in this sector unless the window runs past it;
+        // records after the sentinel belong to the next list and are not read
+        int f = 4;
+#pragma unroll
+        for (int k = 3; k >= 0; --k)
+            if (a4 + k >= b && id[k] > hi) f = k;
+        if (f == 4) return hi;
+        uint32_t li = 0;
+#pragma unroll
+        for (int k = 0; k < 3; k++)
+            if (k + 1 == f && a4 + k >= b) li = id[k];
+        return li;
     }
 
     // next/end: this warp's claimed root slots (u32: n_roots <= m < 2^31)
@@ -920,7 +932,10 @@ struct Warp {
         } else if constexpr (LM > 1) {
             const uint32_t phi[2] = {a, bb};
             const uint32_t hi = ok ? __ldg(p.H + r) : 0;   // t' = t_root + δ as an index
-            push<1>(ok, r, hi, phi, eh, (uint32_t)slot);
+            uint32_t li = ~0u;
+            if constexpr (Layout<Plan, MODE>::look())
+                if (ok) li = look_ahead(r, hi);
+            push<1>(ok, r, hi, phi, eh, (uint32_t)slot, li);
         }
         return true;
     }
@@ -958,7 +973,7 @@ struct Warp {
 
         uint32_t phi[S + 1];
         uint32_t eh[LV + 1];
-        uint32_t hi = 0, rslot = 0, e = 0, w = 0;
+        uint32_t hi = 0, rslot = 0, e = 0, w = 0, li = ~0u;
         bool ok = false;
         if (active) {
             sfor<S>([&](auto kc) {
@@ -967,6 +982,7 @@ struct Warp {
                 else phi[k] = 0u;
             });
             if constexpr (Lay::khi(LV)) hi = fld<LV, Lay::hi(LV)>()[jt];
+            if constexpr (Lay::kli(LV)) li = fld<LV, Lay::li(LV)>()[jt];
             sfor<LV>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
                 if constexpr (Lay::keh_load(LV, k)) eh[k] = fld<LV, Lay::eh(LV, k)>()[jt];
@@ -1041,7 +1057,7 @@ struct Warp {
                 for (int k = 0; k < S2; k++)
                     if (k == nb) phi2[k] = w;
             }
-            push<LV + 1>(ok, e, hi, phi2, eh, rslot);
+            push<LV + 1>(ok, e, hi, phi2, eh, rslot, li);
         }
     }
 

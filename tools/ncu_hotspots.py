@@ -7,7 +7,7 @@ import sys
 
 rep, kre = sys.argv[1], sys.argv[2]
 N = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name",
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name-base", "demangled", "--kernel-name",
                       f"regex:{kre}", "--launch-count", "1"], capture_output=True, text=True).stdout
 lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
@@ -15,7 +15,7 @@ rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
 hdr = rows[0]
 S = hdr.index("Warp Stall Sampling (All Samples)")
 stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_")]
-data = rows[1:]
+data = [r for r in rows[1:] if r and r[0] != "Address" and len(r) == len(hdr) and r[0].startswith("0x")]
 tot = sum(float(r[S] or 0) for r in data)
 agg = {}
 for r in data:
