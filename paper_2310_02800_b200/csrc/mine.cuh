@@ -19,14 +19,20 @@
 // the record array, edge ids only — no timestamps in this kernel: the time
 // bounds are precomputed as horizon indices).  Levels are chosen
 // deepest-first whenever a full 32-candidate batch is available, which keeps
-// every stack within kCap = 64 tasks.
+// every stack within kCap tasks (a level is expanded only while its child
+// stack has room for a full batch of 32 children).
 #pragma once
 
 #include "tm_internal.cuh"
 
 namespace tmg {
 
-constexpr int kCap = 64;             // tasks per level per warp
+#ifndef TM_CAP
+#define TM_CAP 64
+#endif
+constexpr int kCap = TM_CAP;         // tasks per level per warp (>= 33)
+constexpr uint32_t kRoom = kCap - 31;   // a level with fewer tasks takes a batch of 32 children
+static_assert(kCap >= 33 && kCap <= 64, "kCap");
 #ifndef TM_WARPS_PER_BLOCK
 #define TM_WARPS_PER_BLOCK 8
 #endif
@@ -203,6 +209,9 @@ __device__ __forceinline__ void pair_window(const MineParams &p, uint32_t a, uin
     up = first_after32(p.prec, lo, st + len, lim);
 }
 
+// bit of vertex v in a closing look-ahead mask (Fibonacci hashing)
+__device__ __forceinline__ uint32_t look_hash(uint32_t v) { return (v * 0x9E3779B1u) >> 27; }
+
 // saturating arithmetic of the per-level candidate hints (Warp::cand)
 __device__ __forceinline__ uint32_t cand_add(uint32_t c, uint32_t a) { return c > 0x7FFFFFFFu - a ? 0x7FFFFFFFu : c + a; }
 __device__ __forceinline__ uint32_t cand_sub(uint32_t c, uint32_t a) { return c > a ? c - a : 0u; }
@@ -267,16 +276,16 @@ struct Shape {
     // Closing look-ahead.  The last motif edge with both endpoints mapped is
     // an edge between two bound vertices, so it lies in BOTH of their lists
     // (Algorithm 1 may read either, "N_out(u_G)/N_in(v_G)").  The
-    // kernel scans the list of the most recently touched endpoint (ldir);
+    // kernel scans the list of the most recently touched endpoint x (ldir);
     // when the other endpoint y is an endpoint of the root edge (motif vertex
     // 0 or 1), every match's last edge is also a record of y's other-direction
-    // list with id in (e_1, H_δ(e_1)].  The root reads that list's window once
-    // (one rank load, one sector): LI = the id of its last record, 0 when it
-    // is empty, hi when the window runs past the sector (no bound).  Every
-    // closing window is then (e_{L-1}, min(lim, LI)]: empty without a single
-    // load when e_{L-1} >= LI.  The search tree is unchanged (the closing
-    // edge is a leaf), so the counts, the matches and every level's nodes are
-    // Algorithm 1's; only the leaf scans shrink.
+    // list with id in (e_1, H_δ(e_1)], whose neighbour is φ(x).  The root
+    // reads that window once (one rank load, one sector) and keeps a 32-bit
+    // mask of hashed neighbours (0 for an empty window, all ones when the
+    // window runs past the sector).  A closing window whose φ(x) is not in
+    // the mask holds no match and is not read at all.  The search tree is
+    // unchanged (the closing edge is a leaf), so the counts, the matches and
+    // every level's nodes are Algorithm 1's; only leaf scans are skipped.
     __host__ __device__ constexpr int lkdir() const { return 1 - ldir(L - 1); }
     __host__ __device__ constexpr int lky() const { return lkdir() == 0 ? u[L - 1] : v[L - 1]; }
     __host__ __device__ constexpr bool look() const {
@@ -411,9 +420,9 @@ struct Layout {
         return keh(l, k) && !(TM_SIB_LAZY_EH && MODE == kCountSib && l == kSibLevel && k < l && !Plan::keep_eh(l, k));
     }
     __host__ __device__ static constexpr bool khi(int l) { return MODE == kStats || Plan::keep_hi(l); }
-    // the closing look-ahead bound (Shape::look) of the root, carried to level L-2
+    // the closing look-ahead mask (Shape::look) of the root, carried to level L-2
     __host__ __device__ static constexpr bool look() { return MODE != kStats && Plan::look(); }
-    __host__ __device__ static constexpr bool kli(int l) { return look() && l >= 1 && l + 3 <= Plan::kL; }
+    __host__ __device__ static constexpr bool kli(int l) { return look() && l >= 1 && l + 2 <= Plan::kL; }
     __host__ __device__ static constexpr int phi(int l, int k) {
         int f = 2;
         for (int i = 0; i < k; i++) f += kphi(l, i) ? 1 : 0;
@@ -604,7 +613,7 @@ struct Warp {
     // matched edges, last edge e, bound vertices phi.  Searches the candidate
     // window of motif edge NL (GetCandidateEdgeList) and pushes the
     // task if the window is non-empty.
-    // li: the root's closing look-ahead bound (Shape::look; ~0u = none).
+    // li: the root's closing look-ahead mask (Shape::look; ~0u = every vertex).
     template <int NL, int NS, int NE>
     __device__ __forceinline__ void push(bool ok, uint32_t e, uint32_t hi, const uint32_t (&phi)[NS],
                                          const uint32_t (&eh)[NE], uint32_t rslot, uint32_t li = ~0u) {
@@ -618,10 +627,13 @@ struct Warp {
                 if (lane == 0 && c) atomicAdd(p.scratch + kPrefixBase + NL, (unsigned long long)c);
             }
         }
-        // closing edge under the look-ahead: hi is min(H_δ(e_1), LI); a match's
-        // last edge would have to lie in (e, hi], none does when e >= hi
+        // closing edge under the look-ahead: φ(x) must be a neighbour in y's root window
         bool live = ok;
-        if constexpr (Lay::look() && NL + 1 == Plan::kL) live = ok && e < hi;
+        if constexpr (Lay::look() && NL + 1 == Plan::kL)
+            live = ok && ((li >> look_hash(pick(phi, plan.template lx<NL>()))) & 1u);
+#ifdef TM_SKIP_LEAF   // timing experiment only (wrong counts): the cost of the closing level
+        if constexpr (NL + 1 == Plan::kL && MODE != kStats) live = false;
+#endif
         if (live) {
             const uint32_t *hf = p.Hf[NL - 1];
             uint32_t lim = hi;   // min(t_root + δ, t_prev + δ_i) as an id; H_δi read when needed
@@ -814,10 +826,7 @@ struct Warp {
                 constexpr int k = decltype(kc)::value;
                 if constexpr (Lay::kphi(NL, k)) fld<NL, Lay::phi(NL, k)>()[slot] = phi[k < NS ? k : 0];
             });
-            if constexpr (Lay::khi(NL)) {   // level L-2: hi only bounds the closing window
-                if constexpr (Lay::look() && NL + 2 == Plan::kL) fld<NL, Lay::hi(NL)>()[slot] = min(hi, li);
-                else fld<NL, Lay::hi(NL)>()[slot] = hi;
-            }
+            if constexpr (Lay::khi(NL)) fld<NL, Lay::hi(NL)>()[slot] = hi;
             if constexpr (Lay::kli(NL)) fld<NL, Lay::li(NL)>()[slot] = li;
             sfor<NL>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
@@ -863,30 +872,28 @@ struct Warp {
         push<NL>(ok, eh[NL - 1], hi, phi, eh, slot);
     }
 
-    // The closing look-ahead bound of root r (Shape::look): the id of the
-    // last record of y's list in (r, hi], 0 if there is none, hi if that
-    // window runs past the aligned sector holding its start (no gallop: an
-    // upper bound is as correct, only less selective).
+    // The closing look-ahead mask of root r (Shape::look): the hashed
+    // neighbours of y's list records in (r, hi]; 0 if there is none, all ones
+    // if that window runs past the aligned sector holding its start (no
+    // gallop: a superset is as correct, only less selective).
     __device__ __forceinline__ uint32_t look_ahead(uint32_t r, uint32_t hi) const {
         const uint32_t b = __ldg(p.rank + (size_t)Plan::lkvar() * p.m + r);   // first record after r
         const uint32_t a4 = b & ~3u;
         const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(p.rec + a4);
         const ulonglong2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
-        const uint32_t id[4] = {(uint32_t)(x0.x >> 32), (uint32_t)(x0.y >> 32), (uint32_t)(x1.x >> 32),
-                                (uint32_t)(x1.y >> 32)};
-        // the first record past hi: ids ascend up to the list's sentinel (id
-        // 0xFFFFFFFF), so it is in this sector unless the window runs past it;
-        // records after the sentinel belong to the next list and are not read
-        int f = 4;
+        const uint64_t r4[4] = {x0.x, x0.y, x1.x, x1.y};
+        // ids ascend up to the list's sentinel (id 0xFFFFFFFF > hi): the window
+        // ends in this sector unless its last record is still <= hi; records
+        // after the first one past hi belong to the window's end or the next list
+        uint32_t mask = 0;
+        bool end = false;
 #pragma unroll
-        for (int k = 3; k >= 0; --k)
-            if (a4 + k >= b && id[k] > hi) f = k;
-        if (f == 4) return hi;
-        uint32_t li = 0;
-#pragma unroll
-        for (int k = 0; k < 3; k++)
-            if (k + 1 == f && a4 + k >= b) li = id[k];
-        return li;
+        for (int k = 0; k < 4; k++) {
+            if (a4 + k < b || end) continue;
+            if ((uint32_t)(r4[k] >> 32) > hi) end = true;
+            else mask |= 1u << look_hash((uint32_t)r4[k]);
+        }
+        return end ? mask : ~0u;
     }
 
     // next/end: this warp's claimed root slots (u32: n_roots <= m < 2^31)
@@ -1322,14 +1329,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (MinBlocks<Plan, MODE>::v
         // deepest level with a full batch whose child stack has room
 #pragma unroll
         for (int l = LM - 1; l >= 1; --l)
-            if (sel < 0 && l < L && W.cand[l] >= 32 && (l == L - 1 || W.ntask[l + 1 <= LM ? l + 1 : LM] < 32)) sel = l;
+            if (sel < 0 && l < L && W.cand[l] >= 32 && (l == L - 1 || W.ntask[l + 1 <= LM ? l + 1 : LM] < kRoom)) sel = l;
         if (sel < 0) {
-            if (roots_left && (L == 1 || W.ntask[1] < 32)) {
+            if (roots_left && (L == 1 || W.ntask[1] < kRoom)) {
                 sel = 0;
             } else {
 #pragma unroll
                 for (int l = LM - 1; l >= 1; --l)
-                    if (sel < 0 && l < L && W.ntask[l] > 0 && (l == L - 1 || W.ntask[l + 1 <= LM ? l + 1 : LM] < 32)) sel = l;
+                    if (sel < 0 && l < L && W.ntask[l] > 0 && (l == L - 1 || W.ntask[l + 1 <= LM ? l + 1 : LM] < kRoom)) sel = l;
             }
         }
         if (sel < 0) {

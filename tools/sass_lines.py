@@ -15,7 +15,7 @@ rep, kre, obj, msub = sys.argv[1:5]
 obj = os.path.abspath(obj)
 N = int(sys.argv[5]) if len(sys.argv) > 5 else 25
 SKIP = sys.argv[6] if len(sys.argv) > 6 else "0"   # launches of KERNEL_REGEX to skip
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name",
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name-base", "demangled", "--kernel-name",
                       f"regex:{kre}", "--launch-skip", SKIP, "--launch-count", "1"], capture_output=True, text=True).stdout
 lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
@@ -23,7 +23,7 @@ rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
 hdr = rows[0]
 COL = sys.argv[7] if len(sys.argv) > 7 else "Warp Stall Sampling (All Samples)"
 S = hdr.index(COL)
-data = [r for r in rows[1:] if r and r[0].startswith("0x")]
+data = [r for r in rows[1:] if r and r[0].startswith("0x") and len(r) == len(hdr)]
 base = int(data[0][0], 16)
 samples = [(int(r[0], 16) - base, float((r[S] or "0").replace(",", "")), r[1].strip()) for r in data]
 # line table
