@@ -525,8 +525,14 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             max_useful = (max_useful + kWarpsPerBlock - 1) / kWarpsPerBlock;
             grid = std::max<uint64_t>(1, std::min(grid, max_useful));
             // heavy-subtree sharing: idle warps wait for work, so every CTA must
-            // be resident at once (a CTA waiting for a slot would never start)
-            if (p.share != 1) {
+            // be resident at once (a CTA waiting for a slot would never start):
+            // the grid is capped at the co-resident limit and launched
+            // cooperatively, which the driver either schedules all at once or
+            // refuses (cudaErrorCooperativeLaunchTooLarge) — two sharing kernels
+            // on different streams can then never each hold part of the GPU
+            // while waiting for the rest
+            const bool coop = p.share != 1;
+            if (coop) {
                 grid = std::min<uint64_t>(grid, (uint64_t)sms * per_sm);
                 p.total_warps = (uint32_t)(grid * kWarpsPerBlock);
                 uint32_t q = 32;
@@ -547,9 +553,13 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             cfg.blockDim = dim3(threads);
             cfg.dynamicSmemBytes = smem;
             cfg.stream = s;
-            cfg.numAttrs = 0;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = coop ? 1 : 0;
             if (rfn) {
-                TM_CUDA_TRY(rtc_launch(rfn, (unsigned)grid, threads, smem, s, p));
+                TM_CUDA_TRY(rtc_launch(rfn, (unsigned)grid, threads, smem, s, p, coop));
             } else {
                 TM_CUDA_TRY(cudaLaunchKernelEx(&cfg, ki.fn, p));
             }

@@ -45,6 +45,8 @@ struct Driver {
     CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int *, CUfunction, int, size_t) = nullptr;
     CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                              CUstream, void **, void **) = nullptr;
+    CUresult (*LaunchCooperativeKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                        unsigned, CUstream, void **) = nullptr;
     bool ok = false;
 };
 
@@ -64,7 +66,7 @@ const Driver &drv() {
                entry("cuModuleGetFunction", x.ModuleGetFunction) && entry("cuModuleGetGlobal", x.ModuleGetGlobal) &&
                entry("cuMemcpyDtoH", x.MemcpyDtoH) && entry("cuFuncSetAttribute", x.FuncSetAttribute) &&
                entry("cuOccupancyMaxActiveBlocksPerMultiprocessor", x.OccupancyMaxActiveBlocksPerMultiprocessor) &&
-               entry("cuLaunchKernel", x.LaunchKernel);
+               entry("cuLaunchKernel", x.LaunchKernel) && entry("cuLaunchCooperativeKernel", x.LaunchCooperativeKernel);
         return x;
     }();
     return d;
@@ -186,10 +188,14 @@ cudaError_t rtc_occupancy(void *fn, int threads, size_t smem, int *per_sm) {
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-cudaError_t rtc_launch(void *fn, unsigned grid, int threads, size_t smem, cudaStream_t s, const MineParams &p) {
+cudaError_t rtc_launch(void *fn, unsigned grid, int threads, size_t smem, cudaStream_t s, const MineParams &p,
+                       bool coop) {
     void *args[] = {const_cast<MineParams *>(&p)};
-    const CUresult r = drv().LaunchKernel((CUfunction)fn, grid, 1, 1, threads, 1, 1, (unsigned)smem, (CUstream)s,
-                                          args, nullptr);
+    const CUresult r = coop ? drv().LaunchCooperativeKernel((CUfunction)fn, grid, 1, 1, threads, 1, 1, (unsigned)smem,
+                                                            (CUstream)s, args)
+                            : drv().LaunchKernel((CUfunction)fn, grid, 1, 1, threads, 1, 1, (unsigned)smem,
+                                                 (CUstream)s, args, nullptr);
+    if (r == CUDA_ERROR_COOPERATIVE_LAUNCH_TOO_LARGE) return cudaErrorCooperativeLaunchTooLarge;
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
 }
 

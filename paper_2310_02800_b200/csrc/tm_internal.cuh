@@ -291,7 +291,9 @@ struct RtcKernel {
 tm_status rtc_kernel(uint64_t code, bool gen, int mode, RtcKernel *out);
 cudaError_t rtc_set_smem(void *fn, int bytes);
 cudaError_t rtc_occupancy(void *fn, int threads, size_t smem, int *per_sm);
-cudaError_t rtc_launch(void *fn, unsigned grid, int threads, size_t smem, cudaStream_t s, const MineParams &p);
+// coop: a cooperative launch (every CTA resident at once, or the launch fails)
+cudaError_t rtc_launch(void *fn, unsigned grid, int threads, size_t smem, cudaStream_t s, const MineParams &p,
+                       bool coop);
 
 // catalog lookup: specialised kernel for `code` in `mode`, else the generic one
 KernelInfo lookup_kernel(uint64_t code, int mode, bool *specialised, bool generic = false);

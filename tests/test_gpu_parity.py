@@ -775,3 +775,108 @@ def test_fusion_keeps_sibling_carrier():
         assert all(e > 0 for e in exp)
         assert T.tm_count_multi(g, mos) == exp, specs
         assert T.tm_count_multi(g, mos, fuse=1) == exp, specs
+
+
+# --------------------------------------- hardening and invariants
+@pytest.mark.timeout(300)
+def test_concurrent_sharing_kernels_on_two_streams():
+    """tmotif.h allows concurrent tm_count calls on different streams.  The
+    heavy-subtree sharing kernels need every CTA resident (idle warps wait for
+    hand-overs), so they launch cooperatively: two of them started from two
+    host threads on two streams, each filling the GPU, must both finish with
+    the oracle's counts (no partial residency deadlock)."""
+    import threading
+    import torch
+    src, dst, t, n = synth.burst_graph(231002806)
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n)
+    cases = [(M.C4, None), (M.TT, None), (M.TRI, None), (M.P3, [600, 600])]
+    exp = [og.mine(mm, 3600, f)["count"] for mm, f in cases]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    out = [[None] * len(cases) for _ in range(2)]
+    errs = []
+
+    def worker(k):
+        try:
+            for rep in range(3):
+                for i, (mm, f) in enumerate(cases):
+                    out[k][i] = T.tm_count(g, T.Motif(mm, 3600, f), stream=streams[k], share=2 if k else 0)
+        except Exception as ex:   # surfaced below
+            errs.append(ex)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=240)
+    assert not any(x.is_alive() for x in th), "concurrent sharing kernels did not finish"
+    assert not errs, errs
+    assert out[0] == exp and out[1] == exp
+
+
+def test_C4_delta_sweeps_monotone():
+    """SURVEY §8(c) pin 2 at config scale, on the GPU alone: the bench query's
+    counts never decrease as δ grows (δ_i fixed) or as every δ_i grows
+    (δ fixed), and δ_i >= δ equals the coarse-only query."""
+    src, dst, t, n = synth.config_graph("C4")
+    g = T.Graph(src, dst, t, n)
+    prev = None
+    for d in (0, 3600, 21600, 43200, 86400, 2 * 86400):
+        c = T.tm_count_multi(g, [T.Motif(M.get(nm), d, f) for nm, f in C4_BENCH])
+        if prev is not None:
+            assert all(a <= b for a, b in zip(prev, c)), (d, prev, c)
+        prev = c
+    prev = None
+    for fi in (0, 600, 3600, 21600, 86400):
+        c = T.tm_count_multi(g, [T.Motif(M.get(nm), 86400, [fi] * (len(M.get(nm)) - 1)) for nm, _ in C4_BENCH])
+        if prev is not None:
+            assert all(a <= b for a, b in zip(prev, c)), (fi, prev, c)
+        prev = c
+    coarse = T.tm_count_multi(g, [T.Motif(M.get(nm), 86400) for nm, _ in C4_BENCH])
+    assert prev == coarse   # δ_i = δ: the gap bounds are implied by the window
+
+
+def test_C4_bench_query_partitions_agree():
+    """SURVEY §8(c) pin 2 / §8(e): the bench query split for 1, 2, 4 and 8
+    ranks — contiguous root ranges from tm_partition_plan, each rank's slice
+    (roots + forward δ-halo) built as its own graph and mined
+    fused — sums to the same counts (a match belongs to the rank holding e_1)."""
+    src, dst, t, n = synth.config_graph("C4")
+    g = T.Graph(src, dst, t, n)
+    S, D, Tt = g.sorted_edges()
+    g.close()
+    from paper_2310_02800_b200 import multi
+    reach = max(multi.reach(86400, f) for _, f in C4_BENCH)
+    totals = []
+    for P in (1, 2, 4, 8):
+        acc = np.zeros(len(C4_BENCH), np.int64)
+        for r in range(P):
+            a, b, e = multi.rank_slice(Tt, reach, P, r)
+            gp = T.Graph(S[a:e], D[a:e], Tt[a:e], n)
+            acc += np.array(T.tm_count_multi(gp, _bench_query(), root_range=(0, b - a)), np.int64)
+            gp.close()
+        totals.append(acc.tolist())
+    assert all(x == totals[0] for x in totals), totals
+
+
+def test_C5_slice_sampled_roots_specialised():
+    """BASELINE configs[4] (C5, 2e9 edges) is mined as time slices with δ-halos:
+    on one slice, 16 random root ranges of 4096 roots (2^16 roots) through the
+    specialised fused kernels the C5 bench times (TRI as the 4-cycle's sibling
+    rows) against the oracle over the same roots, and the slice's full count
+    against the generic kernel's per-root counts."""
+    s, d, t, n, nr = synth.c5_rank_slice(3, 64, 3600)
+    g = T.Graph(s, d, t, n)
+    og = oracle.Graph(s, d, t, n)
+    mos = [T.Motif(M.TRI, 3600), T.Motif(M.C4, 3600)]
+    rng = np.random.default_rng(5)
+    for _ in range(16):
+        lo = int(rng.integers(0, nr - 4096))
+        rr = (lo, lo + 4096)
+        got = T.tm_count_multi(g, mos, root_range=rr)
+        assert [x["kernel_mode"] for x in T.tm_last_kernel_info()] == [T.KMODE_NONE, T.KMODE_COUNT_SIB]
+        exp = [og.mine(mm, 3600, root_range=rr)["count"] for mm in (M.TRI, M.C4)]
+        assert got == exp, (rr, got, exp)
+    full = T.tm_count_multi(g, mos, root_range=(0, nr))
+    allr = np.arange(nr, dtype=np.uint64)
+    assert full == [int(T.tm_count_roots(g, mo, allr).sum()) for mo in mos]
