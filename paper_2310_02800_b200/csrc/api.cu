@@ -17,12 +17,11 @@ namespace tmg {
 tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m, uint32_t n,
                        const tm_graph_opts *o, tm_graph **out);
 void graph_destroy(tm_graph *g);
-cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, uint64_t *scratch, cudaStream_t s);
+cudaError_t build_horizons(const DeviceGraph &d, int64_t d0, int64_t d1, uint32_t *H0, uint32_t *H1, cudaStream_t s);
 cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s,
                         uint4 *W = nullptr);
 cudaError_t build_tie_lo(const DeviceGraph &d, uint32_t *S, cudaStream_t s);
 tm_status set_labels(DeviceGraph &d, const int32_t *vl, const int32_t *el, bool on_device);
-size_t horizon_scratch_words(uint64_t m);
 
 namespace {
 thread_local std::string g_err;
@@ -340,12 +339,10 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
     fr.v.push_back(scratch);
     TM_CUDA_TRY(cudaMemsetAsync(scratch, 0, (size_t)k * kScratchWords * sizeof(unsigned long long), s));
     uint32_t *hbuf = nullptr, *hrbuf = nullptr;
-    uint64_t *hscr = nullptr;
+    const uint64_t mh = (m + 3) & ~3ull;   // horizon stride: 16-byte aligned arrays (vector stores)
     if (!hv.empty()) {
-        TM_CUDA_TRY(dev_alloc((void **)&hbuf, hv.size() * m * sizeof(uint32_t), s));
+        TM_CUDA_TRY(dev_alloc((void **)&hbuf, hv.size() * mh * sizeof(uint32_t), s));
         fr.v.push_back(hbuf);
-        TM_CUDA_TRY(dev_alloc((void **)&hscr, horizon_scratch_words(m) * sizeof(uint64_t), s));
-        fr.v.push_back(hscr);
     }
     const size_t hr_elem = TM_HRANK == 3 ? sizeof(uint4) : sizeof(uint32_t);
     if (!hkeys.empty()) {
@@ -359,8 +356,9 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
     }
 
     TM_CUDA_TRY(cudaEventRecord(ev0, s));
-    for (size_t i = 0; i < hv.size(); i++) {
-        TM_CUDA_TRY(build_horizon(d, hv[i], hbuf + i * m, hscr, s));
+    for (size_t i = 0; i < hv.size(); i += 2) {   // two horizons per pass (one read of T)
+        const bool two = i + 1 < hv.size();
+        TM_CUDA_TRY(build_horizons(d, hv[i], two ? hv[i + 1] : hv[i], hbuf + i * mh, two ? hbuf + (i + 1) * mh : nullptr, s));
         g_info.launches += 2;
     }
     if (tie) {
@@ -372,7 +370,7 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             TM_CUDA_TRY(cudaMemsetAsync(hrbuf, 0, hkeys.size() * m * sizeof(uint32_t), s));
         } else {
             for (size_t i = 0; i < hkeys.size(); i++) {
-                uint32_t *Hh = hbuf + (size_t)hkeys[i].second * m;
+                uint32_t *Hh = hbuf + (size_t)hkeys[i].second * mh;
                 if (TM_HRANK == 3) {
                     TM_CUDA_TRY(build_hrank(d, hkeys[i].first, Hh, nullptr, s, (uint4 *)hrbuf + i * m));
                 } else {
@@ -462,14 +460,14 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
                 p.anti_u[j] = mo->anti_u[j];
                 p.anti_v[j] = mo->anti_v[j];
                 p.anti_a[j] = mo->anti_attach[j];
-                p.anti_hi[j] = dl[i] >= 0 ? hbuf + (size_t)anti_h[i][j] * m : nullptr;
+                p.anti_hi[j] = dl[i] >= 0 ? hbuf + (size_t)anti_h[i][j] * mh : nullptr;
             }
             p.tie_lo = tie;
         }
         if (dl[i] >= 0) {
-            p.H = hbuf + (size_t)dl[i] * m;
+            p.H = hbuf + (size_t)dl[i] * mh;
             for (uint32_t j = 0; j + 1 < mo->L; j++) {
-                p.Hf[j] = gap[i][j] >= 0 ? hbuf + (size_t)gap[i][j] * m : nullptr;
+                p.Hf[j] = gap[i][j] >= 0 ? hbuf + (size_t)gap[i][j] * mh : nullptr;
                 if (TM_HRANK == 3)
                     p.HW[j] = hwhich[i][j] >= 0 ? (const uint4 *)hrbuf + (size_t)hwhich[i][j] * m : nullptr;
                 else
@@ -979,7 +977,7 @@ tm_status tm_census36(const tm_graph *g, int64_t delta, const int64_t *fine, con
     }
     unsigned long long *dcounts = nullptr;
     uint32_t *hbuf = nullptr;
-    uint64_t *hscr = nullptr;
+    const uint64_t mh = (m + 3) & ~3ull;   // horizon stride: 16-byte aligned arrays (vector stores)
     TM_CUDA_TRY(dev_alloc((void **)&dcounts, 36 * sizeof(unsigned long long), s));
     struct Free {
         void *a, *b, *c;
@@ -993,17 +991,17 @@ tm_status tm_census36(const tm_graph *g, int64_t delta, const int64_t *fine, con
     struct EvFree { cudaEvent_t *e; ~EvFree() { for (int i = 0; i < 4; i++) if (e[i]) cudaEventDestroy(e[i]); } } evf{ev};
     TM_CUDA_TRY(cudaEventRecord(ev[0], s));
     if (p.n_roots > 0) {
-        TM_CUDA_TRY(dev_alloc((void **)&hbuf, hv.size() * m * sizeof(uint32_t), s));
+        TM_CUDA_TRY(dev_alloc((void **)&hbuf, hv.size() * mh * sizeof(uint32_t), s));
         fr.b = hbuf;
-        TM_CUDA_TRY(dev_alloc((void **)&hscr, horizon_scratch_words(m) * sizeof(uint64_t), s));
-        fr.c = hscr;
-        for (size_t i = 0; i < hv.size(); i++) {
-            TM_CUDA_TRY(build_horizon(d, hv[i], hbuf + i * m, hscr, s));
+        for (size_t i = 0; i < hv.size(); i += 2) {
+            const bool two = i + 1 < hv.size();
+            TM_CUDA_TRY(build_horizons(d, hv[i], two ? hv[i + 1] : hv[i], hbuf + i * mh,
+                                       two ? hbuf + (i + 1) * mh : nullptr, s));
             g_info.launches += 2;
         }
         p.H = hbuf;
-        p.Hf0 = gi[0] >= 0 ? hbuf + (size_t)gi[0] * m : nullptr;
-        p.Hf1 = gi[1] >= 0 ? hbuf + (size_t)gi[1] * m : nullptr;
+        p.Hf0 = gi[0] >= 0 ? hbuf + (size_t)gi[0] * mh : nullptr;
+        p.Hf1 = gi[1] >= 0 ? hbuf + (size_t)gi[1] * mh : nullptr;
     }
     TM_CUDA_TRY(cudaEventRecord(ev[1], s));
     if (p.n_roots > 0) {

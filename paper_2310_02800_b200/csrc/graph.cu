@@ -22,6 +22,20 @@ __global__ void k_validate(const uint32_t *src, const uint32_t *dst, const int64
     }
 }
 
+// the id checks of k_validate only (flags[0]); flags[1], flags[2] from k_validate_t
+__global__ void k_validate_ids(const uint32_t *src, const uint32_t *dst, uint64_t m, uint32_t n,
+                               unsigned long long *flags) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        if (src[i] >= n || dst[i] >= n) flags[0] = 1;
+}
+
+__global__ void k_validate_t(const int64_t *t, uint64_t m, unsigned long long *flags) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (t[i] < 0) flags[1] = 1;
+        if (i + 1 < m && t[i] > t[i + 1]) flags[2] = 1;
+    }
+}
+
 __global__ void k_iota(uint32_t *a, uint64_t m) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
         a[i] = (uint32_t)i;
@@ -58,7 +72,7 @@ __global__ void k_bias(uint32_t *off, uint32_t n1, uint32_t bias) {
 #define TM_HB 512
 #endif
 constexpr int kHB = TM_HB;          // edges per block
-constexpr int kHStage = 6 * kHB;    // staged timestamps (24 KB at 512)
+constexpr int kHEpt = 4;            // consecutive edges per thread
 
 __device__ __forceinline__ uint64_t horizon_one(const int64_t *__restrict__ T, uint64_t m, int64_t d, uint64_t e) {
     const int64_t te = T[e];
@@ -79,66 +93,108 @@ __device__ __forceinline__ uint64_t horizon_one(const int64_t *__restrict__ T, u
     return lo - 1;
 }
 
-// H at the first and last edge of every kHB block (one thread each)
-__global__ void k_horizon_ends(const int64_t *__restrict__ T, uint64_t m, int64_t d, uint64_t *__restrict__ ends) {
+// H at the first and last edge of every kHB block, per horizon (one thread each)
+__global__ void k_horizon_ends(const int64_t *__restrict__ T, uint64_t m, int64_t d0, int64_t d1, int nh,
+                               uint64_t *__restrict__ ends) {
     const uint64_t nb = (m + kHB - 1) / kHB;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 2 * nb; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t b = i >> 1;
-        const uint64_t e = (i & 1) ? min((b + 1) * kHB, m) - 1 : b * kHB;
-        ends[i] = horizon_one(T, m, d, e);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 2 * nb * nh;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = i / (2 * nb), r = i - h * 2 * nb, b = r >> 1;
+        const uint64_t e = (r & 1) ? min((b + 1) * kHB, m) - 1 : b * kHB;
+        ends[i] = horizon_one(T, m, h ? d1 : d0, e);
     }
 }
 
-// kHB / kHEpt threads per block, kHEpt edges each (strided for coalescing):
-// the kHEpt branch-free binary searches of a thread are independent, so their
-// shared-memory loads overlap (the kernel is bound by that latency chain).
-#ifndef TM_HORIZON_EPT
-#define TM_HORIZON_EPT 4
-#endif
-constexpr int kHEpt = TM_HORIZON_EPT;
+// Up to two horizons in one pass (the query's δ and its gap bound δ_i share
+// the timestamp reads).  A block takes kHB consecutive edges, kHEpt
+// consecutive edges per thread (one 32-byte load of T, one 16-byte store of
+// H per horizon).  The answer range [H(e0), H(elast)] of each horizon comes
+// from k_horizon_ends (all blocks' gallops in parallel); the block stages T over that range
+// in shared memory (coalesced), and every thread binary-searches its first
+// edge there and walks forward to the next ones (answers are monotone in e:
+// usually a step or two).  Bursty blocks whose range exceeds the stage fall
+// back to the global gallop per edge.
 constexpr int kHThreads = kHB / kHEpt;
+constexpr int kHStage = 6 * kHB;    // staged timestamps per horizon, as u32 offsets from the range's first (12 KB)
 
-__global__ void __launch_bounds__(kHThreads) k_horizon(const int64_t *__restrict__ T, uint64_t m, int64_t d,
-                                                       const uint64_t *__restrict__ ends, uint32_t *__restrict__ H) {
-    __shared__ int64_t st[kHStage];
+template <int NH>
+__global__ void __launch_bounds__(kHThreads) k_horizon(const int64_t *__restrict__ T, uint64_t m, int64_t d0,
+                                                       int64_t d1, const uint64_t *__restrict__ gends,
+                                                       uint32_t *__restrict__ H0, uint32_t *__restrict__ H1) {
+    __shared__ uint32_t st[NH][kHStage];
+    __shared__ uint64_t ends[NH][2];
     const uint64_t e0 = (uint64_t)blockIdx.x * kHB;
     const uint64_t elast = min(e0 + kHB, m) - 1;
-    const uint64_t lo = ends[2 * blockIdx.x], hi = ends[2 * blockIdx.x + 1];   // answers lie in [lo, hi]
-    const uint64_t span = hi - lo + 1;
-    int64_t te[kHEpt];
-#pragma unroll
-    for (int j = 0; j < kHEpt; j++) {
-        const uint64_t e = e0 + threadIdx.x + (uint64_t)j * kHThreads;
-        te[j] = e <= elast ? T[e] : 0;
+    if (threadIdx.x < 2 * NH) {
+        const int h = threadIdx.x >> 1;
+        ends[h][threadIdx.x & 1] = gends[(uint64_t)h * 2 * gridDim.x + 2 * blockIdx.x + (threadIdx.x & 1)];
     }
-    if (span <= kHStage) {
-        for (uint64_t i = threadIdx.x; i < span; i += kHThreads) st[i] = T[lo + i];
-        __syncthreads();
-        // last index with st[idx] <= key; st[0] = T[H(e0)] <= key for every e >= e0
-        uint32_t base[kHEpt];
-        int64_t key[kHEpt];
-#pragma unroll
-        for (int j = 0; j < kHEpt; j++) {
-            base[j] = 0;
-            key[j] = (d == TM_DELTA_INF || te[j] > INT64_MAX - d) ? INT64_MAX : te[j] + d;
-        }
-        for (uint32_t len = (uint32_t)span; len > 1;) {
-            const uint32_t half = len >> 1;
-#pragma unroll
-            for (int j = 0; j < kHEpt; j++)
-                if (st[base[j] + half] <= key[j]) base[j] += half;
-            len -= half;
-        }
-#pragma unroll
-        for (int j = 0; j < kHEpt; j++) {
-            const uint64_t e = e0 + threadIdx.x + (uint64_t)j * kHThreads;
-            if (e <= elast) H[e] = (uint32_t)(key[j] == INT64_MAX ? m - 1 : lo + base[j]);
-        }
+    const uint64_t eb = e0 + (uint64_t)threadIdx.x * kHEpt;   // this thread's first edge
+    int64_t te[kHEpt];
+    if (eb + kHEpt - 1 <= elast) {
+        const longlong2 *v = reinterpret_cast<const longlong2 *>(T + eb);
+        const longlong2 a = v[0], b = v[1];
+        te[0] = a.x; te[1] = a.y; te[2] = b.x; te[3] = b.y;
+        static_assert(kHEpt == 4, "one 32-byte load per thread");
     } else {
 #pragma unroll
-        for (int j = 0; j < kHEpt; j++) {
-            const uint64_t e = e0 + threadIdx.x + (uint64_t)j * kHThreads;
-            if (e <= elast) H[e] = (uint32_t)horizon_one(T, m, d, e);
+        for (int j = 0; j < kHEpt; j++) te[j] = eb + j <= elast ? T[eb + j] : 0;
+    }
+    __syncthreads();
+    // staged: the range fits the stage and spans < 2^32 - 1 time units (u32 offsets)
+    bool staged[NH];
+    int64_t base[NH];
+#pragma unroll
+    for (int h = 0; h < NH; h++) {
+        const uint64_t lo = ends[h][0], span = ends[h][1] - lo + 1;
+        base[h] = T[lo];
+        staged[h] = span <= kHStage && T[ends[h][1]] - base[h] < (int64_t)0xFFFFFFFF;
+        if (staged[h])
+            for (uint64_t i = threadIdx.x; i < span; i += kHThreads) st[h][i] = (uint32_t)(T[lo + i] - base[h]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < NH; h++) {
+        const int64_t d = h ? d1 : d0;
+        uint32_t *H = h ? H1 : H0;
+        const uint64_t lo = ends[h][0], span = ends[h][1] - lo + 1;
+        uint32_t out[kHEpt];
+        if (staged[h]) {
+            const uint32_t *sh = st[h];
+            uint32_t pos = 0;   // last index with sh[pos] <= key; sh[0] = T[H(e0)] <= every key
+#pragma unroll
+            for (int j = 0; j < kHEpt; j++) {
+                const int64_t kf = (d == TM_DELTA_INF || te[j] > INT64_MAX - d) ? INT64_MAX : te[j] + d;
+                // key as an offset from base (>= 0: T[lo] <= key); every staged offset
+                // is < 2^32 - 1, so a key capped there still compares exactly
+                const uint32_t key = (uint32_t)min(kf - base[h], (int64_t)0xFFFFFFFF);
+                // first edge: binary search of [0, span); next ones: gallop from the
+                // previous answer (answers are monotone and usually a step or two apart)
+                uint32_t len;
+                if (j == 0) {
+                    len = (uint32_t)span;
+                } else {
+                    uint32_t step = 1;
+                    while (pos + step < span && sh[pos + step] <= key) { pos += step; step <<= 1; }
+                    len = min(step, (uint32_t)span - pos);   // answer in [pos, pos + len)
+                }
+                while (len > 1) {
+                    const uint32_t half = len >> 1;
+                    if (sh[pos + half] <= key) pos += half;
+                    len -= half;
+                }
+                out[j] = (uint32_t)(kf == INT64_MAX ? m - 1 : lo + pos);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kHEpt; j++) out[j] = eb + j <= elast ? (uint32_t)horizon_one(T, m, d, eb + j) : 0u;
+        }
+        if (eb + kHEpt - 1 <= elast) {
+            *reinterpret_cast<uint4 *>(H + eb) = make_uint4(out[0], out[1], out[2], out[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kHEpt; j++)
+                if (eb + j <= elast) H[eb + j] = out[j];
         }
     }
 }
@@ -281,7 +337,7 @@ cudaError_t dmalloc(T **p, size_t count, cudaStream_t s) {
 
 void free_graph(DeviceGraph &d, cudaStream_t s) {
     for (void *q : {(void *)d.src, (void *)d.dst, (void *)d.t, (void *)d.perm, (void *)d.off_out, (void *)d.off_in,
-                    (void *)d.rec, (void *)d.rank, (void *)d.prec, (void *)d.ptab, (void *)d.pbits,
+                    (void *)d.rec, (void *)d.rank, (void *)d.skip, (void *)d.prec, (void *)d.ptab, (void *)d.pbits,
                     (void *)d.vlab, (void *)d.elab})
         dev_free(q, s);
     d = DeviceGraph{};
@@ -399,16 +455,21 @@ done:
 
 }  // namespace
 
-size_t horizon_scratch_words(uint64_t m) { return 2 * ((m + kHB - 1) / kHB) + 1; }
-
-// H_delta for every edge: two launches (block ends, then the staged search).
-// scratch: horizon_scratch_words(m) u64 of device memory.
-cudaError_t build_horizon(const DeviceGraph &d, int64_t delta, uint32_t *H, uint64_t *scratch, cudaStream_t s) {
+// H_delta for one or two horizons (H1 = nullptr: one), one launch.
+// H arrays are 16-byte aligned (pool allocations of m words, m % 4 == 0 or the tail is scalar).
+cudaError_t build_horizons(const DeviceGraph &d, int64_t d0, int64_t d1, uint32_t *H0, uint32_t *H1, cudaStream_t s) {
     if (!d.m) return cudaSuccess;
-    const uint64_t nb = (d.m + kHB - 1) / kHB;
-    k_horizon_ends<<<grid_for(2 * nb), 256, 0, s>>>(d.t, d.m, delta, scratch);
-    k_horizon<<<(unsigned)nb, kHThreads, 0, s>>>(d.t, d.m, delta, scratch, H);
-    return cudaGetLastError();
+    const unsigned nb = (unsigned)((d.m + kHB - 1) / kHB);
+    const int nh = H1 ? 2 : 1;
+    uint64_t *ends = nullptr;
+    cudaError_t err = dmalloc(&ends, (size_t)2 * nb * nh, s);
+    if (err != cudaSuccess) return err;
+    k_horizon_ends<<<grid_for((uint64_t)2 * nb * nh), 256, 0, s>>>(d.t, d.m, d0, d1, nh, ends);
+    if (H1) k_horizon<2><<<nb, kHThreads, 0, s>>>(d.t, d.m, d0, d1, ends, H0, H1);
+    else k_horizon<1><<<nb, kHThreads, 0, s>>>(d.t, d.m, d0, d0, ends, H0, nullptr);
+    err = cudaGetLastError();
+    dev_free(ends, s);
+    return err;
 }
 
 namespace {
@@ -421,26 +482,43 @@ namespace {
 // per edge and query instead of once per search node (on C4 every edge is
 // e_prev of ~11 nodes).  Gallop from the window start rank[var][e]: windows
 // are δ-short and every list ends in an id-0xFFFFFFFF sentinel.
-// window end of edge e when it lies beyond the first sector: gallop from
-// a (the first unread position), capped at the list's sentinel
-#ifndef TM_HR_STEP0
-#define TM_HR_STEP0 4   // first gallop step (records)
-#endif
-__device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ vtx,
-                                            const uint32_t *__restrict__ offs, uint64_t e, uint32_t a, uint32_t lim) {
-    const uint32_t last = __ldg(offs + vtx[e] + 1) - 1;
-    uint32_t lo = a, step = TM_HR_STEP0, hi = min(lo + TM_HR_STEP0 - 1, last);
-    while ((uint32_t)(__ldg(rec + hi) >> 32) <= lim) {
-        lo = hi + 1;
-        step <<= 1;
-        hi = min(lo + step - 1, last);
+// Window end of an edge whose window runs past the first sector: the first
+// position p >= a (a: the first unread, sector-aligned position) of list x
+// with id > lim.  The skip entries 8j >= a are read a sector (8 entries = 64
+// records) at a time until one lies past the window (or past the list's
+// sentinel at `last`); the answer is then within the 8 records before it:
+// one skip sector + up to three record sectors, issued together, for any
+// window up to 64 records past the first sector.
+__device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ skip,
+                                            const uint32_t *__restrict__ offs, uint32_t x, uint32_t a,
+                                            uint32_t lim) {
+    const uint32_t last = __ldg(offs + x + 1) - 1;   // the list's sentinel
+    uint32_t j = (a + 7) >> 3, jf;
+    for (;;) {
+        const uint32_t jb = j & ~7u;
+        const uint4 s0 = __ldg(reinterpret_cast<const uint4 *>(skip + jb));
+        const uint4 s1 = __ldg(reinterpret_cast<const uint4 *>(skip + jb) + 1);
+        const uint32_t sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+        jf = ~0u;
+#pragma unroll
+        for (int k = 7; k >= 0; --k) {
+            const uint32_t jj = jb + k;
+            if (jj >= j && (8 * jj > last || sv[k] > lim)) jf = jj;
+        }
+        if (jf != ~0u) break;
+        j = jb + 8;
     }
-    while (lo < hi) {   // first id > lim in [lo, hi]; rec[hi] qualifies
-        const uint32_t mid = lo + ((hi - lo) >> 1);
-        if ((uint32_t)(__ldg(rec + mid) >> 32) > lim) hi = mid;
-        else lo = mid + 1;
-    }
-    return lo;
+    // rec[8 jf] (or the sentinel) is past the window, rec[8 (jf - 1)] is not (or precedes a)
+    const uint32_t lo = max(a, 8 * (jf - 1)), hi = min(8 * jf, last);
+    const uint32_t a4 = lo & ~3u;
+    const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(rec + a4);
+    const ulonglong2 y0 = __ldg(v), y1 = __ldg(v + 1), y2 = __ldg(v + 2), y3 = __ldg(v + 3);
+    const uint64_t r8[8] = {y0.x, y0.y, y1.x, y1.y, y2.x, y2.y, y3.x, y3.y};
+    uint32_t ans = hi;   // rec[hi] qualifies
+#pragma unroll
+    for (int k = 7; k >= 0; --k)
+        if (a4 + k >= lo && a4 + k <= hi && (uint32_t)(r8[k] >> 32) > lim) ans = a4 + k;
+    return ans;
 }
 
 #ifndef TM_HR_UNROLL
@@ -448,53 +526,14 @@ __device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, co
 #endif
 constexpr int kHrUnroll = TM_HR_UNROLL;   // edges per thread in flight (independent load chains)
 
-// Warp-cooperative long path (TM_HRANK_WARP_LONG): the lanes whose window
-// runs past the first sector are served one at a time by the whole warp,
-// 32 records per coalesced load, up to kHrWarpIters loads, then the gallop.
-// Must be reached by all 32 lanes (no lane may have left the loop).
-#ifndef TM_HRANK_2PHASE
-#define TM_HRANK_2PHASE 0   // measured slower: 4.71 vs 2.56 ms (profiles/r01_experiments.md)
-#endif
-#ifndef TM_HRANK_WARP_LONG
-#define TM_HRANK_WARP_LONG 0   // measured slower: 3.86 vs 2.66 ms (profiles/r01_experiments.md)
-#endif
-constexpr int kHrWarpIters = 4;
-__device__ __forceinline__ uint32_t hrank_long_warp(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ vtx,
-                                                    const uint32_t *__restrict__ offs, uint64_t e, uint32_t a,
-                                                    uint32_t lim, uint32_t ans) {
-    const int lane = threadIdx.x & 31;
-    unsigned need = __ballot_sync(0xffffffffu, ans == 0xFFFFFFFFu);
-    while (need) {
-        const int src = __ffs(need) - 1;
-        need &= need - 1;
-        const uint64_t es = __shfl_sync(0xffffffffu, e, src);
-        const uint32_t as = __shfl_sync(0xffffffffu, a, src), ls = __shfl_sync(0xffffffffu, lim, src);
-        const uint32_t last = __ldg(offs + vtx[es] + 1) - 1;   // the list's sentinel
-        uint32_t res = 0xFFFFFFFFu, pos = as;
-        for (int it = 0; it < kHrWarpIters && res == 0xFFFFFFFFu; it++, pos += 32) {
-            const uint32_t q = pos + lane;
-            const bool over = q > last || (uint32_t)(__ldg(rec + q) >> 32) > ls;
-            const unsigned m = __ballot_sync(0xffffffffu, over);
-            if (m) res = pos + __ffs(m) - 1;
-        }
-        if (res == 0xFFFFFFFFu && lane == src) res = hrank_long(rec, vtx, offs, es, pos, ls);
-        if (lane == src) ans = res;
-    }
-    return ans;
-}
-
 // R: window-end ranks (u32 per edge), or W: window descriptors {start, end,
 // H[e], 0} (uint4 per edge) when W != nullptr
-__global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ rank,
-                                               const uint32_t *__restrict__ vtx, const uint32_t *__restrict__ offs,
-                                               const uint32_t *__restrict__ H, uint64_t m, uint32_t *__restrict__ R,
-                                               uint4 *__restrict__ W, uint32_t *__restrict__ qe,
-                                               unsigned long long *__restrict__ qn) {
+__global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ skip,
+                                               const uint32_t *__restrict__ rank, const uint32_t *__restrict__ vtx,
+                                               const uint32_t *__restrict__ offs, const uint32_t *__restrict__ H,
+                                               uint64_t m, uint32_t *__restrict__ R, uint4 *__restrict__ W) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    // warp-uniform trip count (the warp long path needs all 32 lanes)
-    const uint64_t lane0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
-    for (uint64_t w0 = lane0; w0 < m; w0 += stride * kHrUnroll) {
-        const uint64_t e0 = w0 + (threadIdx.x & 31u);
+    for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < m; e0 += stride * kHrUnroll) {
         uint32_t lim[kHrUnroll], b[kHrUnroll];
         ulonglong2 x0[kHrUnroll], x1[kHrUnroll];
 #pragma unroll
@@ -514,9 +553,7 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
 #pragma unroll
         for (int u = 0; u < kHrUnroll; u++) {
             const uint64_t e = e0 + u * stride;
-#if !TM_HRANK_WARP_LONG && !TM_HRANK_2PHASE
             if (e >= m) break;
-#endif
             const uint32_t a = b[u] & ~3u;
             const uint32_t id[4] = {(uint32_t)(x0[u].x >> 32), (uint32_t)(x0[u].y >> 32), (uint32_t)(x1[u].x >> 32),
                                     (uint32_t)(x1[u].y >> 32)};
@@ -524,30 +561,17 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
 #pragma unroll
             for (int k = 3; k >= 0; --k)
                 if (a + k >= b[u] && id[k] > lim[u]) ans = a + k;
-#if TM_HRANK_WARP_LONG
-            if (e >= m) ans = 0;   // no edge: not a long-path request
-            ans = hrank_long_warp(rec, vtx, offs, e, a + 4, lim[u], ans);
-            if (e >= m) continue;
-#elif TM_HRANK_2PHASE
-            {   // long windows go to a queue for k_hrank_long (warp-aggregated append)
-                const bool lng = e < m && ans == 0xFFFFFFFFu;
-                const unsigned lm = __ballot_sync(0xffffffffu, lng);
-                if (lm) {
-                    const int lane = threadIdx.x & 31;
-                    unsigned long long base = 0;
-                    if (lane == __ffs(lm) - 1) base = atomicAdd(qn, (unsigned long long)__popc(lm));
-                    base = __shfl_sync(0xffffffffu, base, __ffs(lm) - 1);
-                    if (lng) qe[base + __popc(lm & ((1u << lane) - 1u))] = (uint32_t)e;
-                }
-            }
-            if (e >= m) continue;
-#else
-            if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, vtx, offs, e, a + 4, lim[u]);
-#endif
+            if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, skip, offs, __ldg(vtx + e), a + 4, lim[u]);
             if (W) W[e] = make_uint4(b[u], ans, lim[u], 0u);
             else R[e] = ans;
         }
     }
+}
+
+// skip[j] = id of rec[8j] (Ids past the records: 0xFFFFFFFF)
+__global__ void k_skip(const uint64_t *__restrict__ rec, uint64_t nrec, uint64_t nskip, uint32_t *__restrict__ skip) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nskip; j += (uint64_t)gridDim.x * blockDim.x)
+        skip[j] = 8 * j < nrec ? (uint32_t)(rec[8 * j] >> 32) : 0xFFFFFFFFu;
 }
 }  // namespace
 
@@ -608,50 +632,21 @@ tm_status set_labels(DeviceGraph &d, const int32_t *vl, const int32_t *el, bool 
     return TM_OK;
 }
 
-namespace {
-// Second phase (TM_HRANK_2PHASE): the queued edges whose window runs past the
-// first sector, one per lane, all lanes galloping (no lane waits for a
-// neighbour's long window as in the first phase).
-__global__ void __launch_bounds__(256) k_hrank_long(const uint64_t *__restrict__ rec,
-                                                    const uint32_t *__restrict__ rank,
-                                                    const uint32_t *__restrict__ vtx,
-                                                    const uint32_t *__restrict__ offs,
-                                                    const uint32_t *__restrict__ H, const uint32_t *__restrict__ qe,
-                                                    const unsigned long long *__restrict__ qn,
-                                                    uint32_t *__restrict__ R, uint4 *__restrict__ W) {
-    const unsigned long long n = *qn;
-    for (unsigned long long i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t e = qe[i];
-        const uint32_t ans = hrank_long(rec, vtx, offs, e, (rank[e] & ~3u) + 4, H[e]);
-        if (W) reinterpret_cast<uint32_t *>(W)[4 * (uint64_t)e + 1] = ans;
-        else R[e] = ans;
-    }
-}
-}  // namespace
-
 cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s,
                         uint4 *W) {
     if (!d.m) return cudaSuccess;
     const uint32_t *rk = d.rank + (size_t)var * d.m, *vtx = var < 2 ? d.src : d.dst;
     const uint32_t *offs = (var & 1) ? d.off_in : d.off_out;
-    if (!TM_HRANK_2PHASE) {
-        k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, rk, vtx, offs, H, d.m, R, W, nullptr, nullptr);
-        return cudaGetLastError();
-    }
-    void *q = nullptr;
-    cudaError_t err = dev_alloc(&q, d.m * sizeof(uint32_t) + 16, s);
+    k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, d.skip, rk, vtx, offs, H, d.m, R, W);
+    return cudaGetLastError();
+}
+
+cudaError_t build_skip(DeviceGraph &d, cudaStream_t s) {
+    const uint64_t nskip = (d.nrec + 7) / 8 + 8;   // + a sector of padding for the 8-entry loads
+    cudaError_t err = dmalloc(&d.skip, nskip, s);
     if (err != cudaSuccess) return err;
-    unsigned long long *qn = (unsigned long long *)q;
-    uint32_t *qe = (uint32_t *)((char *)q + 16);
-    err = cudaMemsetAsync(qn, 0, sizeof *qn, s);
-    if (err == cudaSuccess) {
-        k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, rk, vtx, offs, H, d.m, R, W, qe, qn);
-        k_hrank_long<<<grid_for(d.m), 256, 0, s>>>(d.rec, rk, vtx, offs, H, qe, qn, R, W);
-        err = cudaGetLastError();
-    }
-    dev_free(q, s);
-    return err;
+    k_skip<<<grid_for(nskip), 256, 0, s>>>(d.rec, d.nrec, nskip, d.skip);
+    return cudaGetLastError();
 }
 
 tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m, uint32_t n,
@@ -679,27 +674,79 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     TRY(dmalloc(&d.perm, m, s));
     TRY(dmalloc(&d.off_out, (size_t)n + 1, s));
     TRY(dmalloc(&d.off_in, (size_t)n + 1, s));
-    TRY(dmalloc(&d.rec, 2 * (m + n) + 32, s));   // sentinels + padding: warp reads may run 31 records past a sentinel
+    d.nrec = 2 * (m + n);
+    TRY(dmalloc(&d.rec, d.nrec + 32, s));   // sentinels + padding: warp reads may run 31 records past a sentinel
     TRY(cudaMemsetAsync(d.rec, 0xff, (2 * (m + n) + 32) * sizeof(uint64_t), s));
     TRY(dmalloc(&d.rank, 4 * m, s));
     TRY(dmalloc(&flags, 3, s));
-    if (on_dev) {
-        isrc = const_cast<uint32_t *>(src); idst = const_cast<uint32_t *>(dst); it = const_cast<int64_t *>(t);
-    } else {
-        TRY(dmalloc(&isrc, m, s)); TRY(dmalloc(&idst, m, s)); TRY(dmalloc(&it, m, s));
-        if (m) {
-            TRY(cudaMemcpyAsync(isrc, src, m * 4, cudaMemcpyHostToDevice, s));
-            TRY(cudaMemcpyAsync(idst, dst, m * 4, cudaMemcpyHostToDevice, s));
-            TRY(cudaMemcpyAsync(it, t, m * 8, cudaMemcpyHostToDevice, s));
-        }
-    }
     TRY(cudaMemsetAsync(flags, 0, 3 * sizeof(unsigned long long), s));
-    if (m) k_validate<<<grid_for(m), 256, 0, s>>>(isrc, idst, it, m, n, flags);
-    TRY(cudaGetLastError());
-    TRY(cudaMemcpyAsync(hflags, flags, sizeof hflags, cudaMemcpyDeviceToHost, s));
-    TRY(cudaStreamSynchronize(s));
-    if (hflags[0]) { st = fail(TM_EINVAL, "edge endpoint >= n_vertices"); goto fail_free; }
-    if (hflags[1]) { st = fail(TM_EINVAL, "negative timestamp"); goto fail_free; }
+    if (!on_dev && m) {
+        // Host input, pipelined (DESIGN.md §6 "Graph build"): src/dst are copied
+        // straight into place on a copy stream, then t; the CSR is built from
+        // src/dst while t is still in flight, on the guess that the input is
+        // already in time order (edge id = input position).  t's check then
+        // confirms the guess; otherwise the edges are sorted and the CSR is
+        // built again (the result is the same either way).
+        cudaStream_t cs = nullptr;
+        cudaEvent_t ev_sd = nullptr, ev_t = nullptr;
+        struct Own {
+            cudaStream_t &cs; cudaEvent_t &a, &b;
+            ~Own() {   // a failed call may leave copies in flight: they finish before anything is freed
+                if (cs) { cudaStreamSynchronize(cs); cudaStreamDestroy(cs); }
+                if (a) cudaEventDestroy(a);
+                if (b) cudaEventDestroy(b);
+            }
+        } own{cs, ev_sd, ev_t};
+        TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        TRY(cudaEventCreateWithFlags(&ev_sd, cudaEventDisableTiming));
+        TRY(cudaEventCreateWithFlags(&ev_t, cudaEventDisableTiming));
+        TRY(cudaEventRecord(ev_sd, s));            // the allocations above, in stream order
+        TRY(cudaStreamWaitEvent(cs, ev_sd, 0));
+        TRY(cudaMemcpyAsync(d.src, src, m * 4, cudaMemcpyHostToDevice, cs));
+        TRY(cudaMemcpyAsync(d.dst, dst, m * 4, cudaMemcpyHostToDevice, cs));
+        TRY(cudaEventRecord(ev_sd, cs));
+        TRY(cudaMemcpyAsync(d.t, t, m * 8, cudaMemcpyHostToDevice, cs));
+        TRY(cudaEventRecord(ev_t, cs));
+        TRY(cudaStreamWaitEvent(s, ev_sd, 0));
+        k_validate_ids<<<grid_for(m), 256, 0, s>>>(d.src, d.dst, m, n, flags);
+        TRY(cudaGetLastError());
+        TRY(cudaMemcpyAsync(hflags, flags, sizeof hflags, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+        if (hflags[0]) { cudaStreamSynchronize(cs); st = fail(TM_EINVAL, "edge endpoint >= n_vertices"); goto fail_free; }
+        k_iota<<<grid_for(m), 256, 0, s>>>(d.perm, m);
+        TRY(build_csr(d, s));                        // overlaps the copy of t
+        TRY(cudaStreamWaitEvent(s, ev_t, 0));
+        k_validate_t<<<grid_for(m), 256, 0, s>>>(d.t, m, flags);
+        TRY(cudaGetLastError());
+        TRY(cudaMemcpyAsync(hflags, flags, sizeof hflags, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+        if (hflags[1]) { st = fail(TM_EINVAL, "negative timestamp"); goto fail_free; }
+        if (hflags[2]) {   // not in time order: sort below from copies of the input
+            TRY(dmalloc(&isrc, m, s)); TRY(dmalloc(&idst, m, s)); TRY(dmalloc(&it, m, s));
+            TRY(cudaMemcpyAsync(isrc, d.src, m * 4, cudaMemcpyDeviceToDevice, s));
+            TRY(cudaMemcpyAsync(idst, d.dst, m * 4, cudaMemcpyDeviceToDevice, s));
+            TRY(cudaMemcpyAsync(it, d.t, m * 8, cudaMemcpyDeviceToDevice, s));
+            TRY(cudaMemsetAsync(d.rec, 0xff, (2 * (m + n) + 32) * sizeof(uint64_t), s));
+        } else {
+            TRY(build_skip(d, s));
+            TRY(cudaStreamSynchronize(s));
+            dev_free(flags, s);
+            *out = g;
+            return TM_OK;
+        }
+    } else {
+        if (on_dev) {
+            isrc = const_cast<uint32_t *>(src); idst = const_cast<uint32_t *>(dst); it = const_cast<int64_t *>(t);
+        } else {
+            TRY(dmalloc(&isrc, m, s)); TRY(dmalloc(&idst, m, s)); TRY(dmalloc(&it, m, s));
+        }
+        if (m) k_validate<<<grid_for(m), 256, 0, s>>>(isrc, idst, it, m, n, flags);
+        TRY(cudaGetLastError());
+        TRY(cudaMemcpyAsync(hflags, flags, sizeof hflags, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+        if (hflags[0]) { st = fail(TM_EINVAL, "edge endpoint >= n_vertices"); goto fail_free; }
+        if (hflags[1]) { st = fail(TM_EINVAL, "negative timestamp"); goto fail_free; }
+    }
     if (m) k_iota<<<grid_for(m), 256, 0, s>>>(d.perm, m);
     if (hflags[2]) {
         // stable LSD radix sort on t (t >= 0, so its bit pattern orders as u64):
@@ -718,6 +765,7 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     if (m) k_gather<<<grid_for(m), 256, 0, s>>>(d.perm, isrc, idst, it, m, d.src, d.dst, d.t);
     TRY(cudaGetLastError());
     TRY(build_csr(d, s));
+    TRY(build_skip(d, s));
     if (TM_PAIR_LEAF || TM_PAIR_NONLEAF) TRY(build_pairs(d, s));
     TRY(cudaStreamSynchronize(s));
 #undef TRY

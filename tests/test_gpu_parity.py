@@ -880,3 +880,21 @@ def test_C5_slice_sampled_roots_specialised():
     full = T.tm_count_multi(g, mos, root_range=(0, nr))
     allr = np.arange(nr, dtype=np.uint64)
     assert full == [int(T.tm_count_roots(g, mo, allr).sum()) for mo in mos]
+
+
+def test_wide_timestamp_ranges():
+    """Horizons in nanosecond-like units: a block's staged timestamp range can
+    span more than 2^32 units (u32 offsets cannot hold it; the horizon kernel
+    then searches global memory) next to blocks that fit — counts, per-root
+    counts and enumeration still equal the oracle's."""
+    rng = np.random.default_rng(2024)
+    m, n = 30000, 60
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    t = np.sort(rng.integers(0, 7 * 86400, m)).astype(np.int64) * 1_000_000_000   # seconds -> ns
+    t[m // 2:] += 10 ** 15                                                           # a gap of ~11.6 days
+    t[1000:1300] = t[1000]                                                            # a burst of equal times
+    for motif, delta, fine, rows in ((M.TRI, 3600 * 10 ** 9, None, True),
+                                     (M.C4, 7200 * 10 ** 9, [1800 * 10 ** 9] * 3, True),
+                                     (M.P3, 20000 * 10 ** 9, None, False)):
+        check_case(src, dst, t, n, motif, delta, fine, rows=rows, stats=False, roots=True)
