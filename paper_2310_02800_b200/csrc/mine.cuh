@@ -28,7 +28,8 @@
 namespace tmg {
 
 #ifndef TM_CAP
-#define TM_CAP 64
+#define TM_CAP 48   // measured (C4 bench step, mining kernel): 64: 9.10 ms, 48/44: 8.22, 40: 8.31, 36: 8.60, 33: 9.31 —
+                    // smaller stacks leave more of the SM's 228 KB to L1 (hub lists, descriptors)
 #endif
 constexpr int kCap = TM_CAP;         // tasks per level per warp (>= 33)
 constexpr uint32_t kRoom = kCap - 31;   // a level with fewer tasks takes a batch of 32 children
@@ -634,6 +635,9 @@ struct Warp {
 #ifdef TM_SKIP_LEAF   // timing experiment only (wrong counts): the cost of the closing level
         if constexpr (NL + 1 == Plan::kL && MODE != kStats) live = false;
 #endif
+#ifdef TM_SKIP_LV      // timing experiment only (wrong counts): no tasks at level TM_SKIP_LV and below
+        if constexpr (NL >= TM_SKIP_LV && MODE != kStats) live = false;
+#endif
         if (live) {
             const uint32_t *hf = p.Hf[NL - 1];
             uint32_t lim = hi;   // min(t_root + δ, t_prev + δ_i) as an id; H_δi read when needed
@@ -814,7 +818,7 @@ struct Warp {
                 if (leaf && done) lo = up = 0;              // fully scanned
             }
         }
-        const bool keep = ok && up > lo;
+        const bool keep = live && up > lo;
         const uint32_t mask = __ballot_sync(kFull, keep);
         if (!mask) return;
         if (keep) {
@@ -1331,7 +1335,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (MinBlocks<Plan, MODE>::v
         for (int l = LM - 1; l >= 1; --l)
             if (sel < 0 && l < L && W.cand[l] >= 32 && (l == L - 1 || W.ntask[l + 1 <= LM ? l + 1 : LM] < kRoom)) sel = l;
         if (sel < 0) {
-            if (roots_left && (L == 1 || W.ntask[1] < kRoom)) {
+            // a root batch pushes at level 1 (kResume: at the rows' level)
+            uint32_t nroot = W.ntask[1];
+            if (MODE == kResume) {
+#pragma unroll
+                for (int l = 2; l < LM; l++)
+                    if (l == (int)p.resume_level) nroot = W.ntask[l];
+            }
+            if (roots_left && (L == 1 || nroot < kRoom)) {
                 sel = 0;
             } else {
 #pragma unroll
