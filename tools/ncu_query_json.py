@@ -16,13 +16,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2310_02800_b200 import motifs as M  # noqa: E402
 
-METRICS = {"gpu__time_duration.sum": "time_ns", "dram__bytes_read.sum": "dram_read",
+METRICS = {"gpu__time_duration.sum": "time_ms", "dram__bytes_read.sum": "dram_read",
            "dram__bytes_write.sum": "dram_write", "smsp__inst_executed.sum": "warp_inst",
            "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
            "lts__t_sector_hit_rate.pct": "l2_hit_pct", "sm__warps_active.avg.pct_of_peak_sustained_active":
            "occupancy_pct", "smsp__thread_inst_executed_per_inst_executed.ratio": "threads_per_inst",
            "launch__registers_per_thread": "regs"}
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6,
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1,
+         "ns": 1e-6, "us": 1e-3, "ms": 1, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
          "inst": 1, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9}
 
 
@@ -59,14 +60,14 @@ def main(rep, out=os.path.join(ROOT, "profiles", "ncu_traffic.json"), note=""):
                 except ValueError:
                     pass
         k["dram_bytes"] = k.pop("dram_read", 0) + k.pop("dram_write", 0)
-        mm = re.search(r"PlanC<(\d+)ul?, (?:false|0)>, (\d+)>", name.replace("(unsigned long)", ""))
+        mm = re.search(r"PlanC<(\d+)(?:ul?)?, (?:false|0)>, (\d+)>", name.replace("(unsigned long)", ""))
         if mm:
             k["motif"] = CODES.get(int(mm.group(1)), mm.group(1))
             k["mode"] = MODES.get(int(mm.group(2)), mm.group(2))
         kernels.append(k)
     doc = {"config": "C4", "round": 2, "kernels": kernels,
            "query_dram_bytes": sum(k["dram_bytes"] for k in kernels),
-           "query_time_ns_serialised": sum(k.get("time_ns", 0) for k in kernels),
+           "query_time_ms_serialised": sum(k.get("time_ms", 0) for k in kernels),
            "source": "ncu --set full --clock-control none --import-source on -k regex:'mine_kernel|k_horizon|k_hrank' "
                      "python tools/ncu_step.py (one bench query on C4); " + note}
     json.dump(doc, open(out, "w"), indent=1)
