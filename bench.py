@@ -328,9 +328,10 @@ def main():
         src, dst, t, n = synth.config_graph(CONFIG)
         m = len(src)
         log(f"[rank {rank}] generated {CONFIG}: m={m} n={n} in {time.time() - t0:.1f}s")
-        if world > 1:   # contiguous root ranges balanced by the δ-window proxy, + forward δ-halo
+        if world > 1:   # contiguous root ranges balanced by a per-root work proxy, + forward δ-halo
             reach = max(multi.reach(DELTA, motif_fine(x)[1]) for x in MOTIFS)
-            a, b, e = multi.rank_slice(t, reach, world, rank)
+            w = multi.root_weights(src, dst, t, DELTA, FINE)
+            a, b, e = multi.rank_slice(t, reach, world, rank, weights=w)
         else:
             a, b, e = 0, m, m
         yield tuple(np.ascontiguousarray(x[a:e]) for x in (src, dst, t)) + (n, (0, b - a))

@@ -27,6 +27,26 @@ def reach(delta: int, fine=None, anti=None) -> int:
     return r
 
 
+def root_weights(src_sorted, dst_sorted, t_sorted, delta: int, fine1=None):
+    """Per-root work proxy for the split ("better: the
+    level-2 window length"; the paper saw static splits by edge count plateau,
+    P:1258): 1 + the number of edges leaving dst(r) in (r, H(r)], H the
+    tighter of δ and the first gap bound δ_1 — the candidate window of the
+    motif edge 1 -> 2 that every bench motif starts with, whose size sets how
+    many level-2 subtrees root r spawns.  Host numpy, sorted edge order."""
+    S = np.asarray(src_sorted, np.int64)
+    D = np.asarray(dst_sorted, np.int64)
+    t = np.asarray(t_sorted, np.int64)
+    m = len(t)
+    ids = np.arange(m, dtype=np.int64)
+    d = int(delta) if fine1 is None else min(int(delta), int(fine1))
+    H = np.searchsorted(t, t + d, side="right") - 1          # last id within the window
+    key = np.sort(S << 32 | ids)                              # out-lists: (source, id) in order
+    lo = np.searchsorted(key, D << 32 | ids, side="right")
+    hi = np.searchsorted(key, D << 32 | H, side="right")
+    return (1 + hi - lo).astype(np.uint64)
+
+
 def rank_slice(t_sorted, reach_s: int, world: int, rank: int, weights=None):
     """(root_lo, root_hi, edge_hi) of `rank`: it mines roots [root_lo, root_hi)
     on the sorted edges [root_lo, edge_hi) (its roots + forward halo)."""

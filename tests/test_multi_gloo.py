@@ -44,9 +44,11 @@ def _worker(rank, world, port, out):
         src, dst, t, n = _graph(coarse)
         order = np.lexsort((np.arange(len(t)), t))        # (t, input position): sorted edge ids
         S, D, Tt = src[order], dst[order], t[order]
-        for name, delta, fine, anti in CASES:
+        for ci, (name, delta, fine, anti) in enumerate(CASES):
             mot = M.get(name)
-            lo, hi, ehi = multi.rank_slice(Tt, multi.reach(delta, fine, anti), world, rank)
+            # every other case splits by the per-root work proxy (bench.py's N>1 split)
+            w = multi.root_weights(S, D, Tt, delta, None if fine is None else fine[0]) if ci % 2 else None
+            lo, hi, ehi = multi.rank_slice(Tt, multi.reach(delta, fine, anti), world, rank, weights=w)
             g = oracle.Graph(S[lo:ehi], D[lo:ehi], Tt[lo:ehi], n)
             counts.append(g.mine(mot, delta, fine, root_range=(0, hi - lo), anti=anti)["count"])
     total = multi.allreduce_counts(counts)
@@ -106,3 +108,20 @@ def test_reach():
     assert multi.reach(100, [80, 80]) == 100
     assert multi.reach(100, [None, 5]) == 100
     assert multi.reach(100, [30, 20], [(0, 1, 0, 40), (1, 2, 1, 70)]) == 120
+
+
+def test_root_weights_brute_force():
+    """multi.root_weights = 1 + |{j in (r, H(r)] : src(j) = dst(r)}|, H the
+    tighter of δ and δ_1 (the window of motif edge 1 -> 2 after the root),
+    checked edge by edge on a graph with equal timestamps."""
+    src, dst, t, n = synth.tiny_graph(77, n=6, m=200, tmax=60)
+    order = np.lexsort((np.arange(len(t)), t))
+    S, D, Tt = src[order], dst[order], t[order]
+    for delta, f1 in ((10, None), (30, 5), (0, None)):
+        w = multi.root_weights(S, D, Tt, delta, f1)
+        d = delta if f1 is None else min(delta, f1)
+        for r in range(len(Tt)):
+            exp = 1 + sum(1 for j in range(r + 1, len(Tt)) if Tt[j] - Tt[r] <= d and S[j] == D[r])
+            assert int(w[r]) == exp, (delta, f1, r)
+    lo, hi = T.tm_partition_plan(Tt, 10, 4, multi.root_weights(S, D, Tt, 10))
+    assert lo[0] == 0 and lo[-1] == len(Tt) and all(lo[i] <= lo[i + 1] for i in range(4))
