@@ -387,8 +387,10 @@ def main():
         def run():
             cs, mm, nl = fn()
             if lockstep:
+                torch.cuda.nvtx.range_push("tm.allreduce_counts")
                 with torch.cuda.stream(stream):
                     cs = multi.allreduce_counts(cs, device=dev)
+                torch.cuda.nvtx.range_pop()
             return cs, mm, nl
         return run
 

@@ -356,6 +356,7 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
     }
 
     TM_CUDA_TRY(cudaEventRecord(ev0, s));
+    NvtxRange nv_passes("tm.query_passes (horizons, window descriptors)");
     for (size_t i = 0; i < hv.size(); i += 2) {   // two horizons per pass (one read of T)
         const bool two = i + 1 < hv.size();
         TM_CUDA_TRY(build_horizons(d, hv[i], two ? hv[i + 1] : hv[i], hbuf + i * mh, two ? hbuf + (i + 1) * mh : nullptr, s));
@@ -425,6 +426,7 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
             TM_CUDA_TRY(cudaEventRecord(evk[i], s));
             continue;
         }
+        NvtxRange nv_mine(resume_of[i] >= 0 ? "tm.mine (resume)" : "tm.mine");
         MineParams p = base;
         p.prefix_mask = pmask[i];
         p.prefix_lv0 = pmask[i] ? (uint32_t)__builtin_ctz(pmask[i]) : 0u;

@@ -651,6 +651,7 @@ cudaError_t build_skip(DeviceGraph &d, cudaStream_t s) {
 
 tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t m, uint32_t n,
                        const tm_graph_opts *o, tm_graph **out) {
+    NvtxRange nv("tm.graph_create");
     cudaStream_t s = o ? (cudaStream_t)o->stream : nullptr;
     const bool on_dev = o && o->input_on_device;
     tm_graph *g = new (std::nothrow) tm_graph();

@@ -12,6 +12,7 @@ typedef unsigned long long uint64_t;
 #define INT64_MAX 9223372036854775807LL
 #else
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <cstdint>
 #include <string>
 #endif
@@ -310,6 +311,15 @@ bool is_specialised(uint64_t code);
 // (horizons, scratch) and repeated graph builds cost no cudaMalloc/cudaFree.
 cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t s);
 void dev_free(void *p, cudaStream_t s);
+
+// NVTX range for profilers (nsys / ncu --nvtx): host-side phase markers of
+// graph build, horizons, window descriptors and each mining launch
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // error plumbing
 void set_error(const std::string &msg);

@@ -898,3 +898,24 @@ def test_wide_timestamp_ranges():
                                      (M.C4, 7200 * 10 ** 9, [1800 * 10 ** 9] * 3, True),
                                      (M.P3, 20000 * 10 ** 9, None, False)):
         check_case(src, dst, t, n, motif, delta, fine, rows=rows, stats=False, roots=True)
+
+
+def test_timed_kernel_node_counts_equal_algorithm1():
+    """The candidate-caching invariant (every window is searched
+    once, when its node is created) on the kernels the bench times, not only
+    on the instrumentation replay: with PATH2 and P3 fused into the 4-cycle's
+    kernel (kCountPfx counts the nodes it creates at levels 2 and 3), those
+    counts equal the oracle's Algorithm 1 search-tree node counts of the
+    4-cycle search, level by level (C3 and C4, with and without gap bounds)."""
+    for cfg, delta, f in (("C3", 86400, None), ("C4", 86400, 21600)):
+        src, dst, t, n = synth.config_graph(cfg)
+        g = T.Graph(src, dst, t, n)
+        og = oracle.Graph(src, dst, t, n)
+        fine = lambda L: None if f is None else [f] * (L - 1)   # noqa: E731
+        got = T.tm_count_multi(g, [T.Motif(M.PATH2, delta, fine(2)), T.Motif(M.P3, delta, fine(3)),
+                                   T.Motif(M.C4, delta, fine(4))])
+        info = T.tm_last_kernel_info()
+        assert info[0]["carried_by"] == 2 and info[1]["carried_by"] == 2, info
+        st = og.mine(M.C4, delta, fine(4))["stats"]
+        assert got[0] == st["nodes"][2] and got[1] == st["nodes"][3], (cfg, got, st["nodes"])
+        assert got[2] == st["matches"]
