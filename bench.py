@@ -402,7 +402,8 @@ def main():
     nofuse_ms = 0.0
     with ClockSampler(local) as clk:
         for pi, (s_src, s_dst, s_t, n, rr) in enumerate(parts()):
-            g = T.Graph(s_src, s_dst, s_t, n, device=local, stream=stream)
+            # C5 (coarse-only, hub-heavy): the pair index counts long closing windows (tm_graph_opts.pair_index)
+            g = T.Graph(s_src, s_dst, s_t, n, device=local, stream=stream, pair_index=CONFIG == "C5")
             for _ in range(args.warmup):
                 step(g, rr)
             if lockstep:
@@ -441,7 +442,7 @@ def main():
                 hs, hd, ht = (x.numpy() for x in ph)
 
                 def e2e_step():
-                    gg = T.Graph(hs, hd, ht, n, device=local, stream=stream)
+                    gg = T.Graph(hs, hd, ht, n, device=local, stream=stream, pair_index=CONFIG == "C5")
                     cs = ([T.tm_count(gg, mo, root_range=rr, stream=stream) for mo in motifs] if args.separate
                   else T.tm_count_multi(gg, motifs, root_range=rr, stream=stream))
                     gg.close()

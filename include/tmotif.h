@@ -63,6 +63,13 @@ typedef struct {
     int device;           /* CUDA device ordinal; -1 = the calling thread's current */
     void *stream;         /* cudaStream_t for the build; NULL = legacy default      */
     int input_on_device;  /* 1: src/dst/t are device pointers; 0: host pointers     */
+    int pair_index;       /* 1: also build the pair index — the edges of every vertex
+                             pair (u, v), time-sorted, behind a hash table.  A closing
+                             motif edge (both endpoints mapped) whose window in
+                             a hub's list runs past 16 records is then counted from it
+                             with two binary searches instead of a scan.  Pays off on
+                             hub-heavy coarse-only queries (C5 slice: 232 -> 169 ms);
+                             costs ~12 ms and 0.75 GB on a 63.5M-edge graph.  0: not built */
 } tm_graph_opts;
 
 /* Load a temporal graph G = {(src[i], dst[i], t[i])}, i < m and

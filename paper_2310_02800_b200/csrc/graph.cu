@@ -149,8 +149,11 @@ __global__ void __launch_bounds__(kHThreads) k_horizon(const int64_t *__restrict
         const uint64_t lo = ends[h][0], span = ends[h][1] - lo + 1;
         base[h] = T[lo];
         staged[h] = span <= kHStage && T[ends[h][1]] - base[h] < (int64_t)0xFFFFFFFF;
-        if (staged[h])
-            for (uint64_t i = threadIdx.x; i < span; i += kHThreads) st[h][i] = (uint32_t)(T[lo + i] - base[h]);
+        if (staged[h]) {   // 32-bit indexing: span <= kHStage
+            const int64_t *Tl = T + lo;
+            const uint32_t sp = (uint32_t)span;
+            for (uint32_t i = threadIdx.x; i < sp; i += kHThreads) st[h][i] = (uint32_t)(Tl[i] - base[h]);
+        }
     }
     __syncthreads();
 #pragma unroll
@@ -730,6 +733,7 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
             TRY(cudaMemsetAsync(d.rec, 0xff, (2 * (m + n) + 32) * sizeof(uint64_t), s));
         } else {
             TRY(build_skip(d, s));
+            if (TM_PAIR_LEAF || TM_PAIR_NONLEAF || TM_PAIR_BUILD || (o && o->pair_index)) TRY(build_pairs(d, s));
             TRY(cudaStreamSynchronize(s));
             dev_free(flags, s);
             *out = g;
@@ -767,7 +771,7 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     TRY(cudaGetLastError());
     TRY(build_csr(d, s));
     TRY(build_skip(d, s));
-    if (TM_PAIR_LEAF || TM_PAIR_NONLEAF) TRY(build_pairs(d, s));
+    if (TM_PAIR_LEAF || TM_PAIR_NONLEAF || TM_PAIR_BUILD || (o && o->pair_index)) TRY(build_pairs(d, s));
     TRY(cudaStreamSynchronize(s));
 #undef TRY
     if (!on_dev) { dev_free(isrc, s); dev_free(idst, s); dev_free(it, s); }

@@ -86,6 +86,9 @@ struct DeviceGraph {
 #ifndef TM_PAIR_NONLEAF
 #define TM_PAIR_NONLEAF 0
 #endif
+#ifndef TM_PAIR_BUILD
+#define TM_PAIR_BUILD 0     // build the pair index with every graph (long closing windows use it)
+#endif
 
 #ifndef TM_BLOOM_K
 #define TM_BLOOM_K 0        // 0: one bit per pair; k > 0: blocked Bloom, k bits in one 32-byte block

@@ -919,3 +919,30 @@ def test_timed_kernel_node_counts_equal_algorithm1():
         st = og.mine(M.C4, delta, fine(4))["stats"]
         assert got[0] == st["nodes"][2] and got[1] == st["nodes"][3], (cfg, got, st["nodes"])
         assert got[2] == st["matches"]
+
+
+def test_pair_index_long_closing_windows():
+    """tm_graph_opts.pair_index: closing edges whose window in a hub's list runs
+    past the in-lane scan are counted from the pair index (two binary searches
+    over the pair's edges).  On a skewed graph (dense bursts: long hub windows)
+    counts and per-root counts equal the oracle's with and without gap bounds
+    (known and unknown window ends), through the specialised and the generic
+    kernels, and the fused C5 query on a C5 slice equals the query without the
+    index."""
+    src, dst, t, n = synth.burst_graph(231002806)
+    og = oracle.Graph(src, dst, t, n)
+    g = T.Graph(src, dst, t, n, pair_index=True)
+    allr = np.arange(len(src), dtype=np.uint64)
+    for name, fine in (("C4", None), ("C4", [900, 900, 900]), ("TRI", None), ("TT2", None),
+                       ("DIA", [None, 900, None, 1800]), ("P3", None)):
+        motif = M.get(name)
+        mo = T.Motif(motif, 3600, fine)
+        exp = og.mine(motif, 3600, fine)["count"]
+        assert T.tm_count(g, mo) == exp, name
+        pr = og.mine(motif, 3600, fine, roots=allr, per_root=True)["per_root"]
+        assert np.array_equal(T.tm_count_roots(g, mo, allr), pr), name
+    s, d, tt, nn, nr = synth.c5_rank_slice(5, 64, 3600)
+    mos = [T.Motif(M.TRI, 3600), T.Motif(M.C4, 3600)]
+    with_idx = T.tm_count_multi(T.Graph(s, d, tt, nn, pair_index=True), mos, root_range=(0, nr))
+    without = T.tm_count_multi(T.Graph(s, d, tt, nn), mos, root_range=(0, nr))
+    assert with_idx == without and with_idx[1] > 0

@@ -15,7 +15,7 @@ rep, kre, obj, msub = sys.argv[1:5]
 obj = os.path.abspath(obj)
 N = int(sys.argv[5]) if len(sys.argv) > 5 else 25
 SKIP = sys.argv[6] if len(sys.argv) > 6 else "0"   # launches of KERNEL_REGEX to skip
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name-base", "demangled", "--kernel-name",
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name-base", os.environ.get("NCU_NAME_BASE", "demangled"), "--kernel-name",
                       f"regex:{kre}", "--launch-skip", SKIP, "--launch-count", "1"], capture_output=True, text=True).stdout
 lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
