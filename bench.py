@@ -448,11 +448,14 @@ def main():
                     gg.close()
                     return cs
 
-                for _ in range(2):   # warm-up: grows the library's memory pool to a graph's size
+                for _ in range(3):   # warm-up: grows the library's memory pool to a graph's size
                     e2e_step()
                 torch.cuda.synchronize()
+                e2e_each = []
                 for _ in range(args.e2e_steps):
-                    e2e_ms += timed(reduced(lambda: (e2e_step(), [], 0)))[0]
+                    e2e_each.append(timed(reduced(lambda: (e2e_step(), [], 0)))[0])
+                e2e_ms += sum(e2e_each)
+                log(f"[rank {rank}] e2e steps (ms): " + " ".join(f"{x:.2f}" for x in e2e_each))
                 h2d += int(sum(x.numel() * x.element_size() for x in ph))
                 del ph, hs, hd, ht
     if world > 1:

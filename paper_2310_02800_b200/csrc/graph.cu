@@ -51,15 +51,6 @@ __global__ void k_gather(const uint32_t *perm, const uint32_t *src, const uint32
     }
 }
 
-__global__ void k_degree(const uint32_t *v, uint64_t m, uint32_t *deg) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
-        atomicAdd(deg + v[i], 1u);
-}
-
-__global__ void k_bias(uint32_t *off, uint32_t n1, uint32_t bias) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n1; i += gridDim.x * blockDim.x) off[i] += bias;
-}
-
 // H_d[e] = max{ j : T[j] <= T[e] + d }  (>= e; m-1 when d = ∞ or saturated).
 // The δ-window t' = t_root + δ of Algorithm 1 and the
 // fine-grained bound t_prev + δ_i become edge-id limits.
@@ -208,17 +199,42 @@ __global__ void __launch_bounds__(kHThreads) k_horizon(const int64_t *__restrict
 // vertex, all edges touching it in id (= time) order; a scan of "is an
 // out-incidence" flags then counts, at every entry, the out- and in-edges of
 // that vertex that come earlier — exactly the list positions and the ranks.
-__global__ void k_incidences(const uint32_t *src, const uint32_t *dst, uint64_t m, uint32_t *key, uint32_t *val) {
+// value = incidence id << 32 | the other endpoint: the sort carries each
+// record's neighbour, so the scatter after it gathers nothing
+__global__ void k_incidences(const uint32_t *src, const uint32_t *dst, uint64_t m, uint32_t *key, uint64_t *val) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 2 * m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t e = i >> 1;
-        key[i] = (i & 1) ? dst[e] : src[e];
-        val[i] = (uint32_t)i;
+        const uint32_t a = src[e], b = dst[e];
+        key[i] = (i & 1) ? b : a;
+        val[i] = (i << 32) | ((i & 1) ? a : b);
     }
 }
 
-__global__ void k_outflag(const uint32_t *val, uint64_t n2, uint32_t *flag) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n2; i += (uint64_t)gridDim.x * blockDim.x)
-        flag[i] = (val[i] & 1u) ? 0u : 1u;
+// start[u] = first sorted incidence of vertex u (2m past the last; vertices
+// without incidences share the next vertex's start)
+__global__ void k_vertex_starts(const uint32_t *kout, uint64_t n2, uint32_t n, uint32_t *start) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n2; i += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t kv = i < n2 ? (int64_t)kout[i] : (int64_t)n;
+        const int64_t kp = i == 0 ? -1 : (int64_t)kout[i - 1];
+        for (int64_t u = kp + 1; u <= kv; u++) start[u] = (uint32_t)i;
+    }
+}
+
+// list starts from the runs of the merged incidence sort: before vertex v's
+// run come outb[start v] out-incidences and the rest are in-incidences
+// (plain offset + v for the out-lists' sentinels, in-lists further shifted by m + n)
+__global__ void k_offsets_from_runs(const uint32_t *start, const uint32_t *outb, uint32_t n, uint64_t m,
+                                    uint32_t *off_out, uint32_t *off_in) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x) {
+        const uint32_t sv = start[v], ob = outb[sv];
+        off_out[v] = ob + v;
+        off_in[v] = (sv - ob) + (uint32_t)(m + n) + v;
+    }
+}
+
+__global__ void k_outflag(const uint64_t *val, uint64_t n2, uint32_t *flag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n2; i += (uint64_t)gridDim.x * blockDim.x)
+        flag[i] = i < n2 && ((val[i] >> 32) & 1u) == 0 ? 1u : 0u;
 }
 
 // off_out / off_in hold the sentinel-adjusted list starts (plain offset + v,
@@ -228,12 +244,14 @@ __global__ void k_outflag(const uint32_t *val, uint64_t n2, uint32_t *flag) {
 // in incidence order and reach rank[] through a radix sort by incidence id
 // (k_rank_from_sorted): scattering them directly as 4-byte random writes
 // measured 12 ms of a 21 ms build on C4.
-__global__ void k_scatter_csr(const uint32_t *key, const uint32_t *val, const uint32_t *outb, const uint32_t *src,
-                              const uint32_t *dst, const uint32_t *off_out, const uint32_t *off_in, uint64_t m,
-                              uint32_t n, uint64_t *rec, unsigned long long *rk) {
+__global__ void k_scatter_csr(const uint32_t *key, const uint64_t *val, const uint32_t *outb,
+                              const uint32_t *off_out, const uint32_t *off_in, uint64_t m, uint32_t n, uint64_t *rec,
+                              unsigned long long *rk, uint32_t *inc) {
     const uint32_t split = (uint32_t)(m + n);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 2 * m; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t v = key[i], ent = val[i], e = ent >> 1;
+        const uint64_t vv = val[i];
+        const uint32_t v = key[i], ent = (uint32_t)(vv >> 32), e = ent >> 1, nbr = (uint32_t)vv;
+        inc[i] = ent;
         const uint32_t so = off_out[v], si = off_in[v];                 // list starts in rec
         const uint64_t seg = (uint64_t)(so - v) + (si - split - v);      // first incidence of v
         const uint32_t ob = outb[i] - outb[seg];                        // out-incidences of v before i
@@ -241,13 +259,13 @@ __global__ void k_scatter_csr(const uint32_t *key, const uint32_t *val, const ui
         uint32_t a, b;
         if ((ent & 1u) == 0) {            // e in OUT(v), v = src(e)
             const uint32_t pos = so + ob;
-            const uint32_t w = dst[e];
+            const uint32_t w = nbr;
             rec[pos] = ((uint64_t)e << 32) | w;
             a = pos + 1;                          // var 0: OUT(src e)
             b = si + ib + (v == w ? 1u : 0u);     // var 1: IN(src e), ids <= e
         } else {                          // e in IN(v), v = dst(e)
             const uint32_t pos = si + ib;
-            rec[pos] = ((uint64_t)e << 32) | src[e];
+            rec[pos] = ((uint64_t)e << 32) | nbr;
             a = pos + 1;                          // var 3: IN(dst e)
             b = so + ob;                          // var 2: OUT(dst e), ids <= e
         }
@@ -267,14 +285,6 @@ __global__ void k_rank_from_sorted(const unsigned long long *rk, uint64_t m, uin
             rank[3 * m + e] = (uint32_t)(v >> 32); // var 3
             rank[2 * m + e] = (uint32_t)v;         // var 2
         }
-    }
-}
-
-// plain exclusive-scan offsets -> sentinel-adjusted list starts
-__global__ void k_adjust_offsets(uint32_t *off_out, uint32_t *off_in, uint32_t n, uint64_t m) {
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x) {
-        off_out[v] += v;
-        off_in[v] += (uint32_t)(m + n) + v;
     }
 }
 
@@ -350,10 +360,11 @@ void free_graph(DeviceGraph &d, cudaStream_t s) {
 cudaError_t build_csr(DeviceGraph &d, cudaStream_t s) {
     const uint64_t m = d.m;
     const uint32_t n = d.n;
-    uint32_t *deg = nullptr, *key = nullptr, *val = nullptr, *kout = nullptr, *vout = nullptr, *flag = nullptr;
+    uint32_t *key = nullptr, *kout = nullptr, *flag = nullptr, *start = nullptr;
+    uint64_t *val = nullptr, *vout = nullptr;
     unsigned long long *rk = nullptr, *rk2 = nullptr;
     void *tmp = nullptr;
-    size_t sort_bytes = 0, scan_bytes = 0, scan2_bytes = 0, sort2_bytes = 0;
+    size_t sort_bytes = 0, scan2_bytes = 0, sort2_bytes = 0;
     cudaError_t err;
     int end_bit = 1;
     while (end_bit < 32 && (1ull << end_bit) < (uint64_t)n) end_bit++;
@@ -361,45 +372,41 @@ cudaError_t build_csr(DeviceGraph &d, cudaStream_t s) {
     int end_bit2 = 1;   // incidence ids 2e + dir < 2m
     while (end_bit2 < 32 && (1ull << end_bit2) < n2) end_bit2++;
 #define TRY(x) do { err = (x); if (err != cudaSuccess) goto done; } while (0)
-    TRY(dmalloc(&deg, 2 * ((size_t)n + 1), s));
     TRY(dmalloc(&key, n2 + 1, s));
     TRY(dmalloc(&val, n2, s));
     TRY(dmalloc(&kout, n2, s));
     TRY(dmalloc(&vout, n2, s));
     TRY(dmalloc(&flag, n2 + 1, s));
+    TRY(dmalloc(&start, (size_t)n + 1, s));
     TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, key, kout, val, vout, (int64_t)n2, 0, end_bit, s));
-    TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, deg, d.off_out, (int64_t)n + 1, s));
     TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan2_bytes, flag, key, (int64_t)n2 + 1, s));
     TRY(dmalloc(&rk, n2, s));
     TRY(dmalloc(&rk2, n2, s));
-    TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort2_bytes, vout, val, rk, rk2, (int64_t)n2, 0, end_bit2, s));
-    TRY(dev_alloc(&tmp, std::max(std::max(sort_bytes, sort2_bytes), std::max(scan_bytes, scan2_bytes)), s));
-    TRY(cudaMemsetAsync(deg, 0, 2 * ((size_t)n + 1) * 4, s));
-    if (m) {
-        k_degree<<<grid_for(m), 256, 0, s>>>(d.src, m, deg);
-        k_degree<<<grid_for(m), 256, 0, s>>>(d.dst, m, deg + n + 1);
-    }
-    TRY(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, deg, d.off_out, (int64_t)n + 1, s));
-    TRY(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, deg + n + 1, d.off_in, (int64_t)n + 1, s));
-    k_adjust_offsets<<<grid_for((uint64_t)n + 1), 256, 0, s>>>(d.off_out, d.off_in, n, m);
-    k_sentinels<<<grid_for(n), 256, 0, s>>>(d.off_out, d.off_in, n, d.rec);
+    TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort2_bytes, flag, kout, rk, rk2, (int64_t)n2, 0, end_bit2, s));
+    TRY(dev_alloc(&tmp, std::max(std::max(sort_bytes, sort2_bytes), scan2_bytes), s));
+    // one stable sort of the 2m incidences by vertex (value: incidence id and
+    // neighbour); the out-flag scan over it gives every list position, rank
+    // value and — at the runs' starts — both offset arrays (no degree pass)
     if (m) {
         k_incidences<<<grid_for(n2), 256, 0, s>>>(d.src, d.dst, m, key, val);
         TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, key, kout, val, vout, (int64_t)n2, 0, end_bit, s));
-        k_outflag<<<grid_for(n2), 256, 0, s>>>(vout, n2, flag);
-        TRY(cudaMemsetAsync(flag + n2, 0, 4, s));
-        TRY(cub::DeviceScan::ExclusiveSum(tmp, scan2_bytes, flag, key, (int64_t)n2 + 1, s));  // key: free after the sort
-        k_scatter_csr<<<grid_for(n2), 256, 0, s>>>(kout, vout, key, d.src, d.dst, d.off_out, d.off_in, m, n,
-                                                   d.rec, rk);
-        // back to incidence order (val is free after the first sort)
-        TRY(cub::DeviceRadixSort::SortPairs(tmp, sort2_bytes, vout, val, rk, rk2, (int64_t)n2, 0, end_bit2, s));
+    }
+    k_outflag<<<grid_for(n2 + 1), 256, 0, s>>>(vout, n2, flag);
+    TRY(cub::DeviceScan::ExclusiveSum(tmp, scan2_bytes, flag, key, (int64_t)n2 + 1, s));  // key: free after the sort
+    k_vertex_starts<<<grid_for(n2 + 1), 256, 0, s>>>(kout, n2, n, start);
+    k_offsets_from_runs<<<grid_for((uint64_t)n + 1), 256, 0, s>>>(start, key, n, m, d.off_out, d.off_in);
+    k_sentinels<<<grid_for(n), 256, 0, s>>>(d.off_out, d.off_in, n, d.rec);
+    if (m) {
+        k_scatter_csr<<<grid_for(n2), 256, 0, s>>>(kout, vout, key, d.off_out, d.off_in, m, n, d.rec, rk, flag);
+        // back to incidence order (flag holds the incidence ids, kout is free)
+        TRY(cub::DeviceRadixSort::SortPairs(tmp, sort2_bytes, flag, kout, rk, rk2, (int64_t)n2, 0, end_bit2, s));
         k_rank_from_sorted<<<grid_for(n2), 256, 0, s>>>(rk2, m, d.rank);
     }
     TRY(cudaGetLastError());
     TRY(cudaStreamSynchronize(s));
 done:
 #undef TRY
-    for (void *q : {(void *)deg, (void *)key, (void *)val, (void *)kout, (void *)vout, (void *)flag, (void *)rk,
+    for (void *q : {(void *)key, (void *)val, (void *)kout, (void *)vout, (void *)flag, (void *)start, (void *)rk,
                     (void *)rk2, tmp})
         dev_free(q, s);
     return err;

@@ -1,5 +1,6 @@
-"""Host-side timing of the end-to-end pieces (graph build from pinned host
-memory, queries) on the bench workload."""
+"""Host-side timing of the end-to-end step pieces exactly as bench.py's e2e
+pass runs them (graph from pinned host memory, the fused query, graph close),
+with the L2 flush and CUDA events of bench.py around the whole step."""
 import os
 import sys
 import time
@@ -17,48 +18,22 @@ src, dst, t, n = synth.config_graph(bench.CONFIG)
 ph = [torch.from_numpy(x).pin_memory() for x in (src, dst, t)]
 hs, hd, ht = (x.numpy() for x in ph)
 s = torch.cuda.Stream()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 mos = [T.Motif(*bench.motif_fine(x)[:1], bench.DELTA, bench.motif_fine(x)[1]) for x in bench.MOTIFS]
-for it in range(4):
-    torch.cuda.synchronize()
+for it in range(6):
+    with torch.cuda.stream(s):
+        flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
     t0 = time.perf_counter()
     g = T.Graph(hs, hd, ht, n, stream=s)
-    torch.cuda.synchronize()
     t1 = time.perf_counter()
-    for mo in mos:
-        T.tm_count(g, mo, stream=s)
+    cs = T.tm_count_multi(g, mos, stream=s)
     t2 = time.perf_counter()
     g.close()
-    torch.cuda.synchronize()
     t3 = time.perf_counter()
-    print(f"build {1e3 * (t1 - t0):.1f} ms  queries {1e3 * (t2 - t1):.1f} ms  destroy {1e3 * (t3 - t2):.1f} ms",
-          file=sys.stderr)
-
-# the same through tm_count_multi, and a graph kept alive in between (as bench.py's timed part)
-keep = T.Graph(hs, hd, ht, n, stream=s)
-for it in range(3):
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    g = T.Graph(hs, hd, ht, n, stream=s)
-    torch.cuda.synchronize()
-    t1 = time.perf_counter()
-    T.tm_count_multi(g, mos, stream=s)
-    t2 = time.perf_counter()
-    g.close()
-    torch.cuda.synchronize()
-    t3 = time.perf_counter()
-    print(f"[multi, another graph resident] build {1e3 * (t1 - t0):.1f} ms  queries {1e3 * (t2 - t1):.1f} ms  "
-          f"destroy {1e3 * (t3 - t2):.1f} ms", file=sys.stderr)
-keep.close()
-for it in range(3):
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    g = T.Graph(hs, hd, ht, n, stream=s)
-    torch.cuda.synchronize()
-    t1 = time.perf_counter()
-    T.tm_count_multi(g, mos, stream=s)
-    t2 = time.perf_counter()
-    g.close()
-    torch.cuda.synchronize()
-    t3 = time.perf_counter()
-    print(f"[multi] build {1e3 * (t1 - t0):.1f} ms  queries {1e3 * (t2 - t1):.1f} ms  destroy {1e3 * (t3 - t2):.1f} ms",
-          file=sys.stderr)
+    e1.record(s)
+    e1.synchronize()
+    t4 = time.perf_counter()
+    print(f"step {e0.elapsed_time(e1):.2f} ms (events)  create {1e3 * (t1 - t0):.1f}  query {1e3 * (t2 - t1):.1f}  "
+          f"close {1e3 * (t3 - t2):.1f}  tail {1e3 * (t4 - t3):.1f} ms  {cs}", file=sys.stderr)
