@@ -353,6 +353,13 @@ void free_graph(DeviceGraph &d, cudaStream_t s) {
                     (void *)d.rec, (void *)d.rank, (void *)d.skip, (void *)d.prec, (void *)d.ptab, (void *)d.pbits,
                     (void *)d.vlab, (void *)d.elab})
         dev_free(q, s);
+    if (d.nxc) {
+        for (int v = 0; v < 4; v++) {
+            dev_free(d.nxc->nx[v], s);
+            if (d.nxc->ev[v]) cudaEventDestroy(d.nxc->ev[v]);
+        }
+        delete d.nxc;
+    }
     d = DeviceGraph{};
 }
 
@@ -537,41 +544,57 @@ __device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, co
 constexpr int kHrUnroll = TM_HR_UNROLL;   // edges per thread in flight (independent load chains)
 
 // R: window-end ranks (u32 per edge), or W: window descriptors {start, end,
-// H[e], 0} (uint4 per edge) when W != nullptr
+// H[e], 0} (uint4 per edge) when W != nullptr.
+// nxr: the first-record ids of this list variant (NextIdCache), if recorded:
+// a window that ends before its first record (nx[e] > H[e], half of all
+// windows on C4) is written without reading any record.  nxw: record them
+// (the id of the record at the window start, from the sector read anyway).
 __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ skip,
                                                const uint32_t *__restrict__ rank, const uint32_t *__restrict__ vtx,
                                                const uint32_t *__restrict__ offs, const uint32_t *__restrict__ H,
-                                               uint64_t m, uint32_t *__restrict__ R, uint4 *__restrict__ W) {
+                                               uint64_t m, uint32_t *__restrict__ R, uint4 *__restrict__ W,
+                                               const uint32_t *__restrict__ nxr, uint32_t *__restrict__ nxw) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < m; e0 += stride * kHrUnroll) {
         uint32_t lim[kHrUnroll], b[kHrUnroll];
+        bool need[kHrUnroll];
         ulonglong2 x0[kHrUnroll], x1[kHrUnroll];
 #pragma unroll
         for (int u = 0; u < kHrUnroll; u++) {
             const uint64_t e = e0 + u * stride;
             lim[u] = e < m ? H[e] : 0u;
             b[u] = e < m ? rank[e] : 0u;   // first record after e
+            need[u] = e < m && (!nxr || __ldg(nxr + e) <= lim[u]);
         }
         // the aligned 32-byte sector (4 records) holding the window start:
         // windows are δ_i-short, so it usually holds the end too
 #pragma unroll
         for (int u = 0; u < kHrUnroll; u++) {
-            const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(rec + (b[u] & ~3u));
-            x0[u] = __ldg(v);
-            x1[u] = __ldg(v + 1);
+            if (need[u]) {
+                const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(rec + (b[u] & ~3u));
+                x0[u] = __ldg(v);
+                x1[u] = __ldg(v + 1);
+            }
         }
 #pragma unroll
         for (int u = 0; u < kHrUnroll; u++) {
             const uint64_t e = e0 + u * stride;
             if (e >= m) break;
-            const uint32_t a = b[u] & ~3u;
-            const uint32_t id[4] = {(uint32_t)(x0[u].x >> 32), (uint32_t)(x0[u].y >> 32), (uint32_t)(x1[u].x >> 32),
-                                    (uint32_t)(x1[u].y >> 32)};
-            uint32_t ans = 0xFFFFFFFFu;
+            uint32_t ans = b[u];   // empty window (its first record is past the bound)
+            if (need[u]) {
+                const uint32_t a = b[u] & ~3u;
+                const uint32_t id[4] = {(uint32_t)(x0[u].x >> 32), (uint32_t)(x0[u].y >> 32),
+                                        (uint32_t)(x1[u].x >> 32), (uint32_t)(x1[u].y >> 32)};
+                ans = 0xFFFFFFFFu;
 #pragma unroll
-            for (int k = 3; k >= 0; --k)
-                if (a + k >= b[u] && id[k] > lim[u]) ans = a + k;
-            if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, skip, offs, __ldg(vtx + e), a + 4, lim[u]);
+                for (int k = 3; k >= 0; --k)
+                    if (a + k >= b[u] && id[k] > lim[u]) ans = a + k;
+                if (nxw) {
+                    const uint32_t o = b[u] & 3u;
+                    nxw[e] = o == 0 ? id[0] : o == 1 ? id[1] : o == 2 ? id[2] : id[3];
+                }
+                if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, skip, offs, __ldg(vtx + e), a + 4, lim[u]);
+            }
             if (W) W[e] = make_uint4(b[u], ans, lim[u], 0u);
             else R[e] = ans;
         }
@@ -642,13 +665,46 @@ tm_status set_labels(DeviceGraph &d, const int32_t *vl, const int32_t *el, bool 
     return TM_OK;
 }
 
+#ifndef TM_NEXT_IDS
+#define TM_NEXT_IDS 1   // record / use the first-record ids (NextIdCache)
+#endif
+std::mutex g_nxc_mu;   // creation of a graph's NextIdCache
+
 cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s,
                         uint4 *W) {
     if (!d.m) return cudaSuccess;
     const uint32_t *rk = d.rank + (size_t)var * d.m, *vtx = var < 2 ? d.src : d.dst;
     const uint32_t *offs = (var & 1) ? d.off_in : d.off_out;
-    k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, d.skip, rk, vtx, offs, H, d.m, R, W);
-    return cudaGetLastError();
+    const uint32_t *nxr = nullptr;
+    uint32_t *nxw = nullptr;
+    cudaError_t err = cudaSuccess;
+    if (TM_NEXT_IDS) {
+        {
+            std::lock_guard<std::mutex> lk(g_nxc_mu);
+            if (!d.nxc) d.nxc = new NextIdCache();
+        }
+        NextIdCache &c = *d.nxc;
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (c.state[var] == 2) {            // recorded by an earlier query (maybe on another stream)
+            err = cudaStreamWaitEvent(s, c.ev[var], 0);
+            if (err != cudaSuccess) return err;
+            nxr = c.nx[var];
+        } else if (c.state[var] == 0) {     // this query records them
+            err = dmalloc(&c.nx[var], d.m, s);
+            if (err == cudaSuccess) err = cudaEventCreateWithFlags(&c.ev[var], cudaEventDisableTiming);
+            if (err != cudaSuccess) return err;
+            nxw = c.nx[var];
+            c.state[var] = 1;
+        }                                   // state 1: another query is recording them: neither
+    }
+    k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, d.skip, rk, vtx, offs, H, d.m, R, W, nxr, nxw);
+    err = cudaGetLastError();
+    if (nxw) {
+        std::lock_guard<std::mutex> lk(d.nxc->mu);
+        if (err == cudaSuccess) err = cudaEventRecord(d.nxc->ev[var], s);
+        d.nxc->state[var] = err == cudaSuccess ? 2 : 1;   // a failed recording is never used
+    }
+    return err;
 }
 
 cudaError_t build_skip(DeviceGraph &d, cudaStream_t s) {

@@ -38,7 +38,13 @@ static_assert(kCap >= 33 && kCap <= 64, "kCap");
 #define TM_WARPS_PER_BLOCK 8
 #endif
 constexpr int kWarpsPerBlock = TM_WARPS_PER_BLOCK;
-constexpr int kRootChunk = 128;      // roots claimed per global atomic
+constexpr int kRootChunk = 128;      // roots claimed per global atomic (large launches)
+// A resume from few rows (~10^5 sibling rows) claims 32 at a time so every
+// warp of the grid gets some: with 128, 216 k diamond rows reach only ~1700
+// of the 5920 warps and the kernel is all tail (DIA 0.41 -> 0.24 ms).
+#ifndef TM_SMALL_CHUNK
+#define TM_SMALL_CHUNK 1
+#endif
 #ifndef TM_SHARE
 #define TM_SHARE 1          // heavy-subtree sharing compiled in (tm_run_opts.share)
 #endif
@@ -944,12 +950,19 @@ struct Warp {
     // next/end: this warp's claimed root slots (u32: n_roots <= m < 2^31)
     __device__ __forceinline__ bool fetch_roots(uint32_t &next, uint32_t &end) {
         if (next >= end) {
+            // rows claimed per atomic when resuming: 32 if the launch has fewer than 4
+            // chunks per warp (the searching kernels keep 128: measured, any run-time
+            // choice there costs the 4-cycle kernel 0.2 ms of code generation)
+            const uint32_t chunk = (MODE == kResume && TM_SMALL_CHUNK &&
+                                    n_items < 4u * kRootChunk * gridDim.x * kWarpsPerBlock)
+                                       ? 32u
+                                       : (uint32_t)kRootChunk;
             unsigned long long b = 0;
-            if (lane == 0) b = atomicAdd(&p.scratch[0], (unsigned long long)kRootChunk);
+            if (lane == 0) b = atomicAdd(&p.scratch[0], (unsigned long long)chunk);
             b = __shfl_sync(kFull, b, 0);
             if (b >= n_items) return false;
             next = (uint32_t)b;
-            end = (uint32_t)min((uint64_t)(b + kRootChunk), (uint64_t)n_items);
+            end = (uint32_t)min((uint64_t)(b + chunk), (uint64_t)n_items);
         }
         const uint32_t slot = next + lane;
         bool ok = slot < end;

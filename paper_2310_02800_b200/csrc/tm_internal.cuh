@@ -14,6 +14,7 @@ typedef unsigned long long uint64_t;
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 #include <cstdint>
+#include <mutex>
 #include <string>
 #endif
 
@@ -43,6 +44,24 @@ constexpr int kMaxV = TM_MAX_VERTICES;   // motif vertices
 //               + dir: 0 OUT(src e) (own), 1 IN(src e), 2 OUT(dst e),
 //               3 IN(dst e) (own).  Turns the lower-bound binary search of
 //               GetCandidateEdgeList into one load.
+// First-record ids per list variant (k_hrank): nx[var][e] = id of the first
+// record after e in list `var` of e (0xFFFFFFFF: none).  A graph property,
+// independent of δ, recorded by the first query that builds window
+// descriptors for that variant (the record sector it reads anyway); later
+// queries skip the record read of every window that ends before it (half of
+// all windows on C4).  State per variant: 0 absent, 1 being filled, 2 ready
+// (ev: the filling kernel's completion, waited on by other streams).
+#ifndef __CUDACC_RTC__
+struct NextIdCache {
+    std::mutex mu;
+    uint32_t *nx[4] = {nullptr, nullptr, nullptr, nullptr};
+    int state[4] = {0, 0, 0, 0};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+#else
+struct NextIdCache;
+#endif
+
 struct DeviceGraph {
     uint64_t m = 0;
     uint32_t n = 0;
@@ -74,6 +93,8 @@ struct DeviceGraph {
     uint32_t fmask = 0;
     // optional labels (tm_graph_set_labels): per vertex, per edge by sorted id
     int32_t *vlab = nullptr, *elab = nullptr;
+    // lazily filled first-record ids (NextIdCache); owned, freed with the graph
+    mutable NextIdCache *nxc = nullptr;
 };
 
 // Which motif edges with both endpoints mapped (closing edges) read

@@ -946,3 +946,42 @@ def test_pair_index_long_closing_windows():
     with_idx = T.tm_count_multi(T.Graph(s, d, tt, nn, pair_index=True), mos, root_range=(0, nr))
     without = T.tm_count_multi(T.Graph(s, d, tt, nn), mos, root_range=(0, nr))
     assert with_idx == without and with_idx[1] > 0
+
+
+def test_next_id_cache_repeated_and_concurrent_queries():
+    """The first query that builds window descriptors for a list variant
+    records each edge's first-record id in that list (a δ-independent graph
+    index, NextIdCache); later queries on the graph skip the record read of
+    windows ending before it.  Queries before and after it is recorded, with
+    other gap bounds, and first queries racing on two streams of fresh graphs
+    all equal the oracle."""
+    import threading
+    import torch
+    src, dst, t, n = synth.config_graph("C3", m=400_000)
+    og = oracle.Graph(src, dst, t, n)
+    cases = [(M.P3, [1800, 1800]), (M.C4, [3600] * 3), (M.TRI, [600, 600]), (M.DIA, [7200] * 4),
+             (M.C4, [1800] * 3)]
+    exp = [og.mine(mm, 86400, f)["count"] for mm, f in cases]
+    g = T.Graph(src, dst, t, n)
+    for rep in range(2):   # rep 0: the first C4-shaped query records the ids; rep 1: all use them
+        assert [T.tm_count(g, T.Motif(mm, 86400, f)) for mm, f in cases] == exp, rep
+    assert T.tm_count_multi(g, [T.Motif(mm, 86400, f) for mm, f in cases]) == exp
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for trial in range(3):
+        g2 = T.Graph(src, dst, t, n)   # nothing recorded yet: both streams race to be first
+        out = [None, None]
+        errs = []
+
+        def worker(k):
+            try:
+                out[k] = [T.tm_count(g2, T.Motif(mm, 86400, f), stream=streams[k]) for mm, f in cases[k::2]]
+            except Exception as ex:   # surfaced below
+                errs.append(ex)
+
+        th = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join(timeout=120)
+        assert not errs, errs
+        assert out[0] == exp[0::2] and out[1] == exp[1::2], trial
