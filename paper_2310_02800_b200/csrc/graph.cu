@@ -63,6 +63,9 @@ __global__ void k_gather(const uint32_t *perm, const uint32_t *src, const uint32
 #define TM_HB 512
 #endif
 constexpr int kHB = TM_HB;          // edges per block
+#ifndef TM_HLIN
+#define TM_HLIN 0   // single steps before the gallop from the previous answer (0: gallop only)
+#endif
 constexpr int kHEpt = 4;            // consecutive edges per thread
 
 __device__ __forceinline__ uint64_t horizon_one(const int64_t *__restrict__ T, uint64_t m, int64_t d, uint64_t e) {
@@ -169,8 +172,18 @@ __global__ void __launch_bounds__(kHThreads) k_horizon(const int64_t *__restrict
                     len = (uint32_t)span;
                 } else {
                     uint32_t step = 1;
-                    while (pos + step < span && sh[pos + step] <= key) { pos += step; step <<= 1; }
-                    len = min(step, (uint32_t)span - pos);   // answer in [pos, pos + len)
+                    int it = 0;
+#if TM_HLIN
+                    // consecutive answers are usually 0-2 apart: up to TM_HLIN single
+                    // steps, then the gallop
+                    while (it < TM_HLIN && pos + 1 < span && sh[pos + 1] <= key) { ++pos; ++it; }
+#endif
+                    if (TM_HLIN && it < TM_HLIN) {
+                        len = 1;   // stopped: sh[pos + 1] > key (or the range ends)
+                    } else {
+                        while (pos + step < span && sh[pos + step] <= key) { pos += step; step <<= 1; }
+                        len = min(step, (uint32_t)span - pos);   // answer in [pos, pos + len)
+                    }
                 }
                 while (len > 1) {
                     const uint32_t half = len >> 1;
@@ -500,46 +513,51 @@ namespace {
 // e_prev of ~11 nodes).  Gallop from the window start rank[var][e]: windows
 // are δ-short and every list ends in an id-0xFFFFFFFF sentinel.
 // Window end of an edge whose window runs past the first sector: the first
-// position p >= a (a: the first unread, sector-aligned position) of list x
-// with id > lim.  The skip entries 8j >= a are read a sector (8 entries = 64
-// records) at a time until one lies past the window (or past the list's
-// sentinel at `last`); the answer is then within the 8 records before it:
-// one skip sector + up to three record sectors, issued together, for any
-// window up to 64 records past the first sector.
+// position p >= a (a: the first unread, sector-aligned position) with id >
+// lim.  The skip entries 8j >= a are read a sector (8 entries = 64 records)
+// at a time until one stops the scan: its id exceeds lim, or its mark bit
+// says a list's sentinel lies in (8 (j - 1), 8 j] (k_skip_marks) — so the
+// scan never needs the list's bound.  The answer is then within the 8
+// records before it: one skip sector + two record sectors, issued one after
+// the other, for any window up to 64 records past the first sector.  A mark
+// at the first entry can belong to the previous list (its sentinel before
+// a): no record of the window exceeds lim there, and the scan goes on.
 __device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ skip,
-                                            const uint32_t *__restrict__ offs, uint32_t x, uint32_t a,
-                                            uint32_t lim) {
-    const uint32_t last = __ldg(offs + x + 1) - 1;   // the list's sentinel
-    uint32_t j = (a + 7) >> 3, jf;
+                                            uint32_t a, uint32_t lim) {
+    constexpr uint32_t kMark = 0x80000000u, kId = 0x7FFFFFFFu;   // ids < 2^31 (TM_MAX_M)
+    uint32_t j = (a + 7) >> 3;
     for (;;) {
-        const uint32_t jb = j & ~7u;
-        const uint4 s0 = __ldg(reinterpret_cast<const uint4 *>(skip + jb));
-        const uint4 s1 = __ldg(reinterpret_cast<const uint4 *>(skip + jb) + 1);
-        const uint32_t sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-        jf = ~0u;
+        uint32_t jf, svf = 0;
+        for (;;) {
+            const uint32_t jb = j & ~7u;
+            const uint4 s0 = __ldg(reinterpret_cast<const uint4 *>(skip + jb));
+            const uint4 s1 = __ldg(reinterpret_cast<const uint4 *>(skip + jb) + 1);
+            const uint32_t sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            jf = ~0u;
 #pragma unroll
-        for (int k = 7; k >= 0; --k) {
-            const uint32_t jj = jb + k;
-            if (jj >= j && (8 * jj > last || sv[k] > lim)) jf = jj;
+            for (int k = 7; k >= 0; --k)
+                if (jb + k >= j && ((sv[k] & kId) > lim || (sv[k] & kMark))) { jf = jb + k; svf = sv[k]; }
+            if (jf != ~0u) break;
+            j = jb + 8;
         }
-        if (jf != ~0u) break;
-        j = jb + 8;
-    }
-    // rec[8 jf] (or the sentinel) is past the window, rec[8 (jf - 1)] is not (or precedes a)
-    const uint32_t lo = max(a, 8 * (jf - 1)), hi = min(8 * jf, last);
-    const uint32_t a4 = lo & ~3u;
-    const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(rec + a4);
-    const ulonglong2 y0 = __ldg(v), y1 = __ldg(v + 1), y2 = __ldg(v + 2), y3 = __ldg(v + 3);
-    const uint64_t r8[8] = {y0.x, y0.y, y1.x, y1.y, y2.x, y2.y, y3.x, y3.y};
-    uint32_t ans = hi;   // rec[hi] qualifies
+        // rec[8 (jf - 1)] is not past the window (or precedes a)
+        const uint32_t lo = max(a, 8 * (jf - 1)), hi = 8 * jf;
+        const uint32_t a4 = lo & ~3u;
+        const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(rec + a4);
+        const ulonglong2 y0 = __ldg(v), y1 = __ldg(v + 1), y2 = __ldg(v + 2), y3 = __ldg(v + 3);
+        const uint64_t r8[8] = {y0.x, y0.y, y1.x, y1.y, y2.x, y2.y, y3.x, y3.y};
+        uint32_t ans = ~0u;
 #pragma unroll
-    for (int k = 7; k >= 0; --k)
-        if (a4 + k >= lo && a4 + k <= hi && (uint32_t)(r8[k] >> 32) > lim) ans = a4 + k;
-    return ans;
+        for (int k = 7; k >= 0; --k)
+            if (a4 + k >= lo && a4 + k < hi && (uint32_t)(r8[k] >> 32) > lim) ans = a4 + k;
+        if (ans != ~0u) return ans;
+        if ((svf & kId) > lim) return hi;   // rec[8 jf] itself (a sentinel reads 0x7FFFFFFF)
+        j = jf + 1;                         // a mark of the previous list's sentinel
+    }
 }
 
 #ifndef TM_HR_UNROLL
-#define TM_HR_UNROLL 4
+#define TM_HR_UNROLL 2
 #endif
 constexpr int kHrUnroll = TM_HR_UNROLL;   // edges per thread in flight (independent load chains)
 
@@ -549,9 +567,11 @@ constexpr int kHrUnroll = TM_HR_UNROLL;   // edges per thread in flight (indepen
 // a window that ends before its first record (nx[e] > H[e], half of all
 // windows on C4) is written without reading any record.  nxw: record them
 // (the id of the record at the window start, from the sector read anyway).
-__global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ skip,
-                                               const uint32_t *__restrict__ rank, const uint32_t *__restrict__ vtx,
-                                               const uint32_t *__restrict__ offs, const uint32_t *__restrict__ H,
+#ifndef TM_HR_MINB
+#define TM_HR_MINB 1
+#endif
+__global__ void __launch_bounds__(256, TM_HR_MINB) k_hrank(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ skip,
+                                               const uint32_t *__restrict__ rank, const uint32_t *__restrict__ H,
                                                uint64_t m, uint32_t *__restrict__ R, uint4 *__restrict__ W,
                                                const uint32_t *__restrict__ nxr, uint32_t *__restrict__ nxw) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -593,7 +613,7 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
                     const uint32_t o = b[u] & 3u;
                     nxw[e] = o == 0 ? id[0] : o == 1 ? id[1] : o == 2 ? id[2] : id[3];
                 }
-                if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, skip, offs, __ldg(vtx + e), a + 4, lim[u]);
+                if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, skip, a + 4, lim[u]);
             }
             if (W) W[e] = make_uint4(b[u], ans, lim[u], 0u);
             else R[e] = ans;
@@ -605,6 +625,16 @@ __global__ void __launch_bounds__(256) k_hrank(const uint64_t *__restrict__ rec,
 __global__ void k_skip(const uint64_t *__restrict__ rec, uint64_t nrec, uint64_t nskip, uint32_t *__restrict__ skip) {
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nskip; j += (uint64_t)gridDim.x * blockDim.x)
         skip[j] = 8 * j < nrec ? (uint32_t)(rec[8 * j] >> 32) : 0xFFFFFFFFu;
+}
+
+// mark bit (bit 31; ids are < 2^31) of skip[j] where a list's sentinel lies in
+// (8 (j - 1), 8 j]: a scan of the skip entries then stops in the list it started in
+__global__ void k_skip_marks(const uint32_t *__restrict__ off_out, const uint32_t *__restrict__ off_in, uint32_t n,
+                             uint32_t *__restrict__ skip) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        atomicOr(skip + ((off_out[v + 1] - 1 + 7) >> 3), 0x80000000u);
+        atomicOr(skip + ((off_in[v + 1] - 1 + 7) >> 3), 0x80000000u);
+    }
 }
 }  // namespace
 
@@ -673,8 +703,7 @@ std::mutex g_nxc_mu;   // creation of a graph's NextIdCache
 cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s,
                         uint4 *W) {
     if (!d.m) return cudaSuccess;
-    const uint32_t *rk = d.rank + (size_t)var * d.m, *vtx = var < 2 ? d.src : d.dst;
-    const uint32_t *offs = (var & 1) ? d.off_in : d.off_out;
+    const uint32_t *rk = d.rank + (size_t)var * d.m;
     const uint32_t *nxr = nullptr;
     uint32_t *nxw = nullptr;
     cudaError_t err = cudaSuccess;
@@ -697,7 +726,7 @@ cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32
             c.state[var] = 1;
         }                                   // state 1: another query is recording them: neither
     }
-    k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, d.skip, rk, vtx, offs, H, d.m, R, W, nxr, nxw);
+    k_hrank<<<grid_for(d.m), 256, 0, s>>>(d.rec, d.skip, rk, H, d.m, R, W, nxr, nxw);
     err = cudaGetLastError();
     if (nxw) {
         std::lock_guard<std::mutex> lk(d.nxc->mu);
@@ -712,6 +741,7 @@ cudaError_t build_skip(DeviceGraph &d, cudaStream_t s) {
     cudaError_t err = dmalloc(&d.skip, nskip, s);
     if (err != cudaSuccess) return err;
     k_skip<<<grid_for(nskip), 256, 0, s>>>(d.rec, d.nrec, nskip, d.skip);
+    if (d.n) k_skip_marks<<<grid_for(d.n), 256, 0, s>>>(d.off_out, d.off_in, d.n, d.skip);
     return cudaGetLastError();
 }
 

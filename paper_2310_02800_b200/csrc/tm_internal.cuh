@@ -71,10 +71,11 @@ struct DeviceGraph {
     uint32_t *off_out = nullptr, *off_in = nullptr;
     uint64_t *rec = nullptr;
     uint32_t *rank = nullptr;
-    // skip[j] = id of rec[8j] (0xFFFFFFFF past the end; +8 entries of padding):
-    // one u32 per 8 records (66 MB on C4, L2-sized), so a window end deep in a
-    // hub's list is found with one skip sector plus one record sector instead
-    // of a gallop over the records (k_hrank)
+    // skip[j] = id of rec[8j] (0xFFFFFFFF past the end; +8 entries of
+    // padding), bit 31 set where a list's sentinel lies in rec(8(j-1), 8j]: one u32
+    // per 8 records (66 MB on C4, L2-sized), so a window end deep in a hub's
+    // list is found with one skip sector plus one record sector instead of a
+    // gallop over the records, and without the list's bound (k_hrank)
     uint32_t *skip = nullptr;
     uint64_t nrec = 0;
     // pair index: prec = edge ids grouped by (src, dst) pair, ascending id in
