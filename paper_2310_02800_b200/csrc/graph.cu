@@ -66,7 +66,14 @@ constexpr int kHB = TM_HB;          // edges per block
 #ifndef TM_HLIN
 #define TM_HLIN 0   // single steps before the gallop from the previous answer (0: gallop only)
 #endif
-constexpr int kHEpt = 4;            // consecutive edges per thread
+#ifndef TM_HEPT
+#define TM_HEPT 4
+#endif
+#ifndef TM_HSTAGE
+#define TM_HSTAGE 6
+#endif
+constexpr int kHEpt = TM_HEPT;      // consecutive edges per thread (4 or 8)
+static_assert(kHEpt == 4 || kHEpt == 8, "kHEpt");
 
 __device__ __forceinline__ uint64_t horizon_one(const int64_t *__restrict__ T, uint64_t m, int64_t d, uint64_t e) {
     const int64_t te = T[e];
@@ -109,7 +116,7 @@ __global__ void k_horizon_ends(const int64_t *__restrict__ T, uint64_t m, int64_
 // usually a step or two).  Bursty blocks whose range exceeds the stage fall
 // back to the global gallop per edge.
 constexpr int kHThreads = kHB / kHEpt;
-constexpr int kHStage = 6 * kHB;    // staged timestamps per horizon, as u32 offsets from the range's first (12 KB)
+constexpr int kHStage = TM_HSTAGE * kHB;   // staged timestamps per horizon, as u32 offsets from the range's first (12 KB)
 
 template <int NH>
 __global__ void __launch_bounds__(kHThreads) k_horizon(const int64_t *__restrict__ T, uint64_t m, int64_t d0,
@@ -127,9 +134,12 @@ __global__ void __launch_bounds__(kHThreads) k_horizon(const int64_t *__restrict
     int64_t te[kHEpt];
     if (eb + kHEpt - 1 <= elast) {
         const longlong2 *v = reinterpret_cast<const longlong2 *>(T + eb);
-        const longlong2 a = v[0], b = v[1];
-        te[0] = a.x; te[1] = a.y; te[2] = b.x; te[3] = b.y;
-        static_assert(kHEpt == 4, "one 32-byte load per thread");
+#pragma unroll
+        for (int q = 0; q < kHEpt / 2; q++) {   // 32-byte loads
+            const longlong2 a = v[q];
+            te[2 * q] = a.x;
+            te[2 * q + 1] = a.y;
+        }
     } else {
 #pragma unroll
         for (int j = 0; j < kHEpt; j++) te[j] = eb + j <= elast ? T[eb + j] : 0;
@@ -197,7 +207,9 @@ __global__ void __launch_bounds__(kHThreads) k_horizon(const int64_t *__restrict
             for (int j = 0; j < kHEpt; j++) out[j] = eb + j <= elast ? (uint32_t)horizon_one(T, m, d, eb + j) : 0u;
         }
         if (eb + kHEpt - 1 <= elast) {
-            *reinterpret_cast<uint4 *>(H + eb) = make_uint4(out[0], out[1], out[2], out[3]);
+#pragma unroll
+            for (int q = 0; q < kHEpt / 4; q++)
+                reinterpret_cast<uint4 *>(H + eb)[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
         } else {
 #pragma unroll
             for (int j = 0; j < kHEpt; j++)
@@ -560,6 +572,10 @@ __device__ __noinline__ uint32_t hrank_long(const uint64_t *__restrict__ rec, co
 #define TM_HR_UNROLL 2
 #endif
 constexpr int kHrUnroll = TM_HR_UNROLL;   // edges per thread in flight (independent load chains)
+#ifndef TM_NEXT_IDS
+#define TM_NEXT_IDS 2   // record / use the first-record ids (NextIdCache): 1 the first, 2 the first two
+#endif
+constexpr bool kNx2 = TM_NEXT_IDS == 2;
 
 // R: window-end ranks (u32 per edge), or W: window descriptors {start, end,
 // H[e], 0} (uint4 per edge) when W != nullptr.
@@ -578,13 +594,25 @@ __global__ void __launch_bounds__(256, TM_HR_MINB) k_hrank(const uint64_t *__res
     for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < m; e0 += stride * kHrUnroll) {
         uint32_t lim[kHrUnroll], b[kHrUnroll];
         bool need[kHrUnroll];
+        uint32_t b1[kHrUnroll];   // known window length when no read is needed (0 or 1)
+#pragma unroll
+        for (int u = 0; u < kHrUnroll; u++) b1[u] = 0u;
         ulonglong2 x0[kHrUnroll], x1[kHrUnroll];
 #pragma unroll
         for (int u = 0; u < kHrUnroll; u++) {
             const uint64_t e = e0 + u * stride;
             lim[u] = e < m ? H[e] : 0u;
             b[u] = e < m ? rank[e] : 0u;   // first record after e
-            need[u] = e < m && (!nxr || __ldg(nxr + e) <= lim[u]);
+            need[u] = e < m;
+            if (nxr && e < m) {
+                if (kNx2) {   // the first two record ids: windows of length 0 and 1 need no read
+                    const uint2 q = __ldg(reinterpret_cast<const uint2 *>(nxr) + e);
+                    need[u] = q.x <= lim[u] && q.y <= lim[u];
+                    if (q.x <= lim[u] && q.y > lim[u]) b1[u] = 1u;
+                } else {
+                    need[u] = __ldg(nxr + e) <= lim[u];
+                }
+            }
         }
         // the aligned 32-byte sector (4 records) holding the window start:
         // windows are δ_i-short, so it usually holds the end too
@@ -600,7 +628,7 @@ __global__ void __launch_bounds__(256, TM_HR_MINB) k_hrank(const uint64_t *__res
         for (int u = 0; u < kHrUnroll; u++) {
             const uint64_t e = e0 + u * stride;
             if (e >= m) break;
-            uint32_t ans = b[u];   // empty window (its first record is past the bound)
+            uint32_t ans = b[u] + b1[u];   // a window of known length 0 or 1 (nx)
             if (need[u]) {
                 const uint32_t a = b[u] & ~3u;
                 const uint32_t id[4] = {(uint32_t)(x0[u].x >> 32), (uint32_t)(x0[u].y >> 32),
@@ -611,7 +639,11 @@ __global__ void __launch_bounds__(256, TM_HR_MINB) k_hrank(const uint64_t *__res
                     if (a + k >= b[u] && id[k] > lim[u]) ans = a + k;
                 if (nxw) {
                     const uint32_t o = b[u] & 3u;
-                    nxw[e] = o == 0 ? id[0] : o == 1 ? id[1] : o == 2 ? id[2] : id[3];
+                    const uint32_t f = o == 0 ? id[0] : o == 1 ? id[1] : o == 2 ? id[2] : id[3];
+                    if (kNx2)   // second id unknown (0) when it lies in the next sector
+                        reinterpret_cast<uint2 *>(nxw)[e] = make_uint2(f, o == 0 ? id[1] : o == 1 ? id[2] : o == 2 ? id[3] : 0u);
+                    else
+                        nxw[e] = f;
                 }
                 if (ans == 0xFFFFFFFFu) ans = hrank_long(rec, skip, a + 4, lim[u]);
             }
@@ -695,9 +727,7 @@ tm_status set_labels(DeviceGraph &d, const int32_t *vl, const int32_t *el, bool 
     return TM_OK;
 }
 
-#ifndef TM_NEXT_IDS
-#define TM_NEXT_IDS 1   // record / use the first-record ids (NextIdCache)
-#endif
+
 std::mutex g_nxc_mu;   // creation of a graph's NextIdCache
 
 cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s,
@@ -719,7 +749,7 @@ cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32
             if (err != cudaSuccess) return err;
             nxr = c.nx[var];
         } else if (c.state[var] == 0) {     // this query records them
-            err = dmalloc(&c.nx[var], d.m, s);
+            err = dmalloc(&c.nx[var], d.m * (kNx2 ? 2 : 1), s);
             if (err == cudaSuccess) err = cudaEventCreateWithFlags(&c.ev[var], cudaEventDisableTiming);
             if (err != cudaSuccess) return err;
             nxw = c.nx[var];
