@@ -227,6 +227,14 @@ __device__ __forceinline__ void pair_window(const MineParams &p, uint32_t a, uin
     up = first_after32(p.prec, lo, st + len, lim);
 }
 
+// records of the root window read for the closing look-ahead mask, from the
+// aligned sector holding the window start (4: one sector, 8 or 12: two or three)
+#ifndef TM_LOOK_RECS
+#define TM_LOOK_RECS 4
+#endif
+constexpr int kLookRecs = TM_LOOK_RECS;
+static_assert(kLookRecs == 4 || kLookRecs == 8 || kLookRecs == 12, "kLookRecs");
+
 // bit of vertex v in a closing look-ahead mask (Fibonacci hashing)
 __device__ __forceinline__ uint32_t look_hash(uint32_t v) { return (v * 0x9E3779B1u) >> 27; }
 
@@ -931,18 +939,24 @@ struct Warp {
         const uint32_t b = __ldg(p.rank + (size_t)Plan::lkvar() * p.m + r);   // first record after r
         const uint32_t a4 = b & ~3u;
         const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(p.rec + a4);
-        const ulonglong2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
-        const uint64_t r4[4] = {x0.x, x0.y, x1.x, x1.y};
+        constexpr int NR = kLookRecs;   // records read from the aligned sector holding b on
+        uint64_t rr[NR];
+#pragma unroll
+        for (int q = 0; q < NR / 2; q++) {
+            const ulonglong2 x = __ldg(vp + q);
+            rr[2 * q] = x.x;
+            rr[2 * q + 1] = x.y;
+        }
         // ids ascend up to the list's sentinel (id 0xFFFFFFFF > hi): the window
-        // ends in this sector unless its last record is still <= hi; records
+        // ends in these records unless the last one is still <= hi; records
         // after the first one past hi belong to the window's end or the next list
         uint32_t mask = 0;
         bool end = false;
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < NR; k++) {
             if (a4 + k < b || end) continue;
-            if ((uint32_t)(r4[k] >> 32) > hi) end = true;
-            else mask |= 1u << look_hash((uint32_t)r4[k]);
+            if ((uint32_t)(rr[k] >> 32) > hi) end = true;
+            else mask |= 1u << look_hash((uint32_t)rr[k]);
         }
         return end ? mask : ~0u;
     }
