@@ -74,6 +74,9 @@ constexpr unsigned kShareSleepMax = TM_SHARE_SLEEP;   // ns, longest back-off of
 #define TM_LEAF_SECTORS 4
 #endif
 constexpr int kLeafSectors = TM_LEAF_SECTORS;
+#ifndef TM_LEAF_TASK
+#define TM_LEAF_TASK 0      // 1: known leaf windows are pushed as tasks instead of scanned in the lane
+#endif
 #ifndef TM_PAIR_LONG
 #define TM_PAIR_LONG 1      // long closing-leaf windows counted from the pair index (when the graph has one)
 #endif
@@ -234,6 +237,17 @@ __device__ __forceinline__ void pair_window(const MineParams &p, uint32_t a, uin
 #endif
 constexpr int kLookRecs = TM_LOOK_RECS;
 static_assert(kLookRecs == 4 || kLookRecs == 8 || kLookRecs == 12, "kLookRecs");
+
+// Per-root arrays (src, dst, H, the look-ahead rank) are read once per root in
+// root order: with TM_STREAM_HINT they are loaded evict-first (ld.global.cs),
+// so they do not push list records and descriptors out of L2
+#ifndef TM_STREAM_HINT
+#define TM_STREAM_HINT 0
+#endif
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t *q) {
+    if (TM_STREAM_HINT) return __ldcs(q);
+    return __ldg(q);
+}
 
 // bit of vertex v in a closing look-ahead mask (Fibonacci hashing)
 __device__ __forceinline__ uint32_t look_hash(uint32_t v) { return (v * 0x9E3779B1u) >> 27; }
@@ -777,7 +791,14 @@ struct Warp {
                         }
                     }
                 }
-                if (leaf && known && !via_pair) {
+                if (TM_LEAF_TASK && leaf && known && !via_pair) {
+                    // timing variant: every non-empty known leaf window becomes a task
+                    // (the warp scans the tasks 32 candidates at a time)
+                    done = up_known <= lo;
+                    pp = lo;
+                    up = up_known;
+                    nsec = 0;
+                } else if (leaf && known && !via_pair) {
                     // the window [lo, up_known) is known: scan only the sectors it covers
                     // (an empty window reads nothing), with no end test per record
                     const int cover = up_known <= lo ? 0 : (int)(((up_known - 1) >> 2) - (lo >> 2)) + 1;
@@ -936,7 +957,7 @@ struct Warp {
     // if that window runs past the aligned sector holding its start (no
     // gallop: a superset is as correct, only less selective).
     __device__ __forceinline__ uint32_t look_ahead(uint32_t r, uint32_t hi) const {
-        const uint32_t b = __ldg(p.rank + (size_t)Plan::lkvar() * p.m + r);   // first record after r
+        const uint32_t b = ld_stream(p.rank + (size_t)Plan::lkvar() * p.m + r);   // first record after r
         const uint32_t a4 = b & ~3u;
         const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(p.rec + a4);
         constexpr int NR = kLookRecs;   // records read from the aligned sector holding b on
@@ -994,8 +1015,8 @@ struct Warp {
         uint32_t r = 0, a = 0, bb = 0;
         if (ok) {
             r = (uint32_t)(p.roots ? p.roots[slot] : p.root_lo + slot);
-            a = __ldg(p.src + r);
-            bb = __ldg(p.dst + r);
+            a = ld_stream(p.src + r);
+            bb = ld_stream(p.dst + r);
             ok = a != bb;   // a self-loop cannot map two distinct motif vertices (Q4)
             if (gen() && ok)
                 ok = labels_ok(0, r, true, 1, bb) && (p.vreq[0] == TM_ANY_LABEL || vlabel(a) == p.vreq[0]);
@@ -1010,7 +1031,7 @@ struct Warp {
             emit(ok, eh, r, (uint32_t)slot);
         } else if constexpr (LM > 1) {
             const uint32_t phi[2] = {a, bb};
-            const uint32_t hi = ok ? __ldg(p.H + r) : 0;   // t' = t_root + δ as an index
+            const uint32_t hi = ok ? ld_stream(p.H + r) : 0;   // t' = t_root + δ as an index
             uint32_t li = ~0u;
             if constexpr (Layout<Plan, MODE>::look())
                 if (ok) li = look_ahead(r, hi);
