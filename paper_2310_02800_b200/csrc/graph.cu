@@ -379,10 +379,9 @@ void free_graph(DeviceGraph &d, cudaStream_t s) {
                     (void *)d.vlab, (void *)d.elab})
         dev_free(q, s);
     if (d.nxc) {
-        for (int v = 0; v < 4; v++) {
-            dev_free(d.nxc->nx[v], s);
+        dev_free(d.nxc->buf, s);
+        for (int v = 0; v < 4; v++)
             if (d.nxc->ev[v]) cudaEventDestroy(d.nxc->ev[v]);
-        }
         delete d.nxc;
     }
     d = DeviceGraph{};
@@ -736,7 +735,6 @@ tm_status set_labels(DeviceGraph &d, const int32_t *vl, const int32_t *el, bool 
 }
 
 
-std::mutex g_nxc_mu;   // creation of a graph's NextIdCache
 
 cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32_t *R, cudaStream_t s,
                         uint4 *W) {
@@ -745,11 +743,7 @@ cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32
     const uint32_t *nxr = nullptr;
     uint32_t *nxw = nullptr;
     cudaError_t err = cudaSuccess;
-    if (TM_NEXT_IDS) {
-        {
-            std::lock_guard<std::mutex> lk(g_nxc_mu);
-            if (!d.nxc) d.nxc = new NextIdCache();
-        }
+    if (TM_NEXT_IDS && d.nxc) {   // allocated with the graph (build_skip)
         NextIdCache &c = *d.nxc;
         std::lock_guard<std::mutex> lk(c.mu);
         if (c.state[var] == 2) {            // recorded by an earlier query (maybe on another stream)
@@ -757,9 +751,6 @@ cudaError_t build_hrank(const DeviceGraph &d, int var, const uint32_t *H, uint32
             if (err != cudaSuccess) return err;
             nxr = c.nx[var];
         } else if (c.state[var] == 0) {     // this query records them
-            err = dmalloc(&c.nx[var], d.m * (kNx2 ? 2 : 1), s);
-            if (err == cudaSuccess) err = cudaEventCreateWithFlags(&c.ev[var], cudaEventDisableTiming);
-            if (err != cudaSuccess) return err;
             nxw = c.nx[var];
             c.state[var] = 1;
         }                                   // state 1: another query is recording them: neither
@@ -778,6 +769,20 @@ cudaError_t build_skip(DeviceGraph &d, cudaStream_t s) {
     const uint64_t nskip = (d.nrec + 7) / 8 + 8;   // + a sector of padding for the 8-entry loads
     cudaError_t err = dmalloc(&d.skip, nskip, s);
     if (err != cudaSuccess) return err;
+    if (TM_NEXT_IDS && d.m) {
+        // the first-record-id cache: allocated here with the graph (one block for
+        // the four list variants, filled by the first query that needs each one);
+        // (2 GB on C4)
+        d.nxc = new NextIdCache();
+        const uint64_t per = d.m * (kNx2 ? 2 : 1);
+        err = dmalloc(&d.nxc->buf, 4 * per, s);
+        if (err != cudaSuccess) return err;
+        for (int v = 0; v < 4; v++) {
+            d.nxc->nx[v] = d.nxc->buf + v * per;
+            err = cudaEventCreateWithFlags(&d.nxc->ev[v], cudaEventDisableTiming);
+            if (err != cudaSuccess) return err;
+        }
+    }
     k_skip<<<grid_for(nskip), 256, 0, s>>>(d.rec, d.nrec, nskip, d.skip);
     if (d.n) k_skip_marks<<<grid_for(d.n), 256, 0, s>>>(d.off_out, d.off_in, d.n, d.skip);
     return cudaGetLastError();
@@ -928,6 +933,10 @@ void graph_destroy(tm_graph *g) {
     cudaSetDevice(g->device);
     cudaDeviceSynchronize();   // no work of any stream may still read the graph
     free_graph(g->d, nullptr);
+    // let the frees complete now: a graph built right after this one (on any
+    // stream) then reuses the pool's memory instead of growing the pool
+    // (measured: e2e steps of 32 ms with occasional 100-600 ms growth spikes)
+    cudaStreamSynchronize(nullptr);
     cudaSetDevice(dev);
     delete g;
 }

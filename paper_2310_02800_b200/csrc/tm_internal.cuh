@@ -44,16 +44,18 @@ constexpr int kMaxV = TM_MAX_VERTICES;   // motif vertices
 //               + dir: 0 OUT(src e) (own), 1 IN(src e), 2 OUT(dst e),
 //               3 IN(dst e) (own).  Turns the lower-bound binary search of
 //               GetCandidateEdgeList into one load.
-// First-record ids per list variant (k_hrank): nx[var][e] = id of the first
-// record after e in list `var` of e (0xFFFFFFFF: none).  A graph property,
-// independent of δ, recorded by the first query that builds window
-// descriptors for that variant (the record sector it reads anyway); later
+// First-record ids per list variant (k_hrank): nx[var][e] = ids of the first
+// two records after e in list `var` of e (0xFFFFFFFF: none; second 0:
+// unknown).  A graph property, independent of δ, allocated with the graph and
+// recorded by the first query that builds window descriptors for that
+// variant (from the record sector it reads anyway); later
 // queries skip the record read of every window that ends before it (half of
 // all windows on C4).  State per variant: 0 absent, 1 being filled, 2 ready
 // (ev: the filling kernel's completion, waited on by other streams).
 #ifndef __CUDACC_RTC__
 struct NextIdCache {
     std::mutex mu;
+    uint32_t *buf = nullptr;   // one block: nx[v] = buf + v * 2m
     uint32_t *nx[4] = {nullptr, nullptr, nullptr, nullptr};
     int state[4] = {0, 0, 0, 0};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
