@@ -68,8 +68,8 @@ def main(rep, out=os.path.join(ROOT, "profiles", "ncu_traffic.json"), note=""):
     doc = {"config": "C4", "round": 2, "kernels": kernels,
            "query_dram_bytes": sum(k["dram_bytes"] for k in kernels),
            "query_time_ms_serialised": sum(k.get("time_ms", 0) for k in kernels),
-           "source": "ncu --set full --clock-control none --import-source on -k regex:'mine_kernel|k_horizon|k_hrank' "
-                     "python tools/ncu_step.py (one bench query on C4); " + note}
+           "source": note or ("ncu --set full --clock-control none --import-source on -k regex:'mine_kernel|k_horizon|k_hrank' "
+                                "python tools/ncu_step.py (one bench query on C4)")}
     json.dump(doc, open(out, "w"), indent=1)
     print(json.dumps(doc, indent=1))
 
