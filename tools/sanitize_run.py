@@ -29,6 +29,8 @@ def main():
     specs = [(M.P3, [1800] * 2), (M.TRI, [1800] * 2), (M.C4, [1800] * 3), (M.DIA, [1800] * 4)]
     got = T.tm_count_multi(g, [T.Motif(mm, 3600, f) for mm, f in specs])
     assert got == [og.mine(mm, 3600, f)["count"] for mm, f in specs], got
+    # again: the window descriptors now use the first-record ids the first query recorded
+    assert T.tm_count_multi(g, [T.Motif(mm, 3600, f) for mm, f in specs]) == got
     assert list(T.tm_census36(g, 3600)) == [og.mine(M.P36[k], 3600)["count"] for k in range(36)]
     allr = np.arange(len(src), dtype=np.uint64)
     pr = T.tm_count_roots(g, T.Motif(M.C4, 3600), allr)
