@@ -74,6 +74,9 @@ constexpr unsigned kShareSleepMax = TM_SHARE_SLEEP;   // ns, longest back-off of
 #define TM_LEAF_SECTORS 4
 #endif
 constexpr int kLeafSectors = TM_LEAF_SECTORS;
+#ifndef TM_PAIR_FILTER
+#define TM_PAIR_FILTER 1    // 1: closing leaves test the pair index's membership filter first (graphs with one)
+#endif
 #ifndef TM_LEAF_TASK
 #define TM_LEAF_TASK 0      // 1: known leaf windows are pushed as tasks instead of scanned in the lane
 #endif
@@ -671,6 +674,16 @@ struct Warp {
         bool live = ok;
         if constexpr (Lay::look() && NL + 1 == Plan::kL)
             live = ok && ((li >> look_hash(pick(phi, plan.template lx<NL>()))) & 1u);
+        if constexpr (TM_PAIR_FILTER && NL + 1 == Plan::kL && MODE != kStats) {
+            // closing leaf on a graph with a pair index: a pair with no edge at all
+            // (the filter's certain "absent") reads no list (the closing edge
+            // is an edge of this very vertex pair)
+            if (plan.template u<NL>() < plan.template nv<NL>() && plan.template v<NL>() < plan.template nv<NL>() &&
+                p.ptab && live && !gen()) {
+                const uint64_t key = ((uint64_t)pick(phi, plan.template u<NL>()) << 32) | pick(phi, plan.template v<NL>());
+                live = pair_maybe(p.pbits, p.fmask, pair_hash(key));
+            }
+        }
 #ifdef TM_SKIP_LEAF   // timing experiment only (wrong counts): the cost of the closing level
         if constexpr (NL + 1 == Plan::kL && MODE != kStats) live = false;
 #endif
