@@ -42,7 +42,11 @@ CONFIGS = {
     "C4": {"motifs": ["P3", "TRI", "C4", "DIA"], "delta": 86400, "fine": 21600, "index": 3},
     "C5": {"motifs": ["TRI", "C4"], "delta": 3600, "fine": None, "index": 4},
 }
-C5_PARTS = 8
+# 128 slices of ~15.6 M edges: per edge, smaller slices mine faster (their
+# lists and pair filter stay closer to L2): a 1/8-slice's worth of roots took
+# 1715 / 1449 / 1242 / 1108 / 1022 ms as 1 / 2 / 4 / 8 / 16 slices
+# (profiles/r02_experiments.md); the forward δ-halo adds 0.4 % edges per slice
+C5_PARTS = 128
 CONFIG = "C4"
 MOTIFS = CONFIGS[CONFIG]["motifs"]
 DELTA = CONFIGS[CONFIG]["delta"]

@@ -575,6 +575,7 @@ constexpr int kHrUnroll = TM_HR_UNROLL;   // edges per thread in flight (indepen
 #define TM_NEXT_IDS 2   // record / use the first-record ids (NextIdCache): 1 the first, 2 the first two
 #endif
 constexpr bool kNx2 = TM_NEXT_IDS == 2;
+constexpr bool kNx4 = TM_NEXT_IDS == 4;
 #ifndef TM_HR_STREAM
 #define TM_HR_STREAM 0   // evict-first loads of the per-edge inputs and stores of the descriptors
 #endif
@@ -607,7 +608,14 @@ __global__ void __launch_bounds__(256, TM_HR_MINB) k_hrank(const uint64_t *__res
             b[u] = e < m ? (TM_HR_STREAM ? __ldcs(rank + e) : rank[e]) : 0u;   // first record after e
             need[u] = e < m;
             if (nxr && e < m) {
-                if (kNx2) {   // the first two record ids: windows of length 0 and 1 need no read
+                if (kNx4) {   // the first four record ids: windows of length 0..3 need no read
+                    const uint4 q = __ldg(reinterpret_cast<const uint4 *>(nxr) + e);
+                    // ids ascend up to the list's sentinel (> lim); anything after the
+                    // first id past lim is not in the window (unknown ids read 0: in it)
+                    const bool i1 = q.x <= lim[u], i2 = i1 && q.y <= lim[u], i3 = i2 && q.z <= lim[u];
+                    need[u] = i3 && q.w <= lim[u];
+                    b1[u] = (uint32_t)i1 + (uint32_t)i2 + (uint32_t)i3;
+                } else if (kNx2) {   // the first two record ids: windows of length 0 and 1 need no read
                     const uint2 q = TM_HR_STREAM ? __ldcs(reinterpret_cast<const uint2 *>(nxr) + e)
                                                  : __ldg(reinterpret_cast<const uint2 *>(nxr) + e);
                     need[u] = q.x <= lim[u] && q.y <= lim[u];
@@ -643,7 +651,11 @@ __global__ void __launch_bounds__(256, TM_HR_MINB) k_hrank(const uint64_t *__res
                 if (nxw) {
                     const uint32_t o = b[u] & 3u;
                     const uint32_t f = o == 0 ? id[0] : o == 1 ? id[1] : o == 2 ? id[2] : id[3];
-                    if (kNx2)   // second id unknown (0) when it lies in the next sector
+                    if (kNx4)   // ids past the sector unknown (0)
+                        reinterpret_cast<uint4 *>(nxw)[e] =
+                            make_uint4(f, o == 0 ? id[1] : o == 1 ? id[2] : o == 2 ? id[3] : 0u,
+                                       o == 0 ? id[2] : o == 1 ? id[3] : 0u, o == 0 ? id[3] : 0u);
+                    else if (kNx2)   // second id unknown (0) when it lies in the next sector
                         reinterpret_cast<uint2 *>(nxw)[e] = make_uint2(f, o == 0 ? id[1] : o == 1 ? id[2] : o == 2 ? id[3] : 0u);
                     else
                         nxw[e] = f;
@@ -774,7 +786,7 @@ cudaError_t build_skip(DeviceGraph &d, cudaStream_t s) {
         // the four list variants, filled by the first query that needs each one);
         // (2 GB on C4)
         d.nxc = new NextIdCache();
-        const uint64_t per = d.m * (kNx2 ? 2 : 1);
+        const uint64_t per = d.m * (kNx4 ? 4 : kNx2 ? 2 : 1);
         err = dmalloc(&d.nxc->buf, 4 * per, s);
         if (err != cudaSuccess) return err;
         for (int v = 0; v < 4; v++) {
