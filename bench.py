@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -80,6 +81,17 @@ def workload_config(world, m=None):
                             f"each slice drawn, built and timed resident in turn")
         cfg["cache"] = "each slice's graph ~17 GB > 126 MB L2; L2 flushed (256 MiB write) between timed steps"
     return cfg
+
+
+def pair_bucket_log2(t_sorted):
+    """C5 graphs: edge-id buckets of the pair filter about two δ-windows wide
+    (2^k >= 2 m δ / span), so a closing window covers at most two of them
+    (C5 1/128 slice: k = 17, 66.2 -> 55.4 ms; profiles/r02_experiments.md)."""
+    if CONFIG != "C5" or len(t_sorted) < 2:
+        return 0
+    span = max(1, int(t_sorted[-1]) - int(t_sorted[0]))
+    per = 2.0 * len(t_sorted) * DELTA / span
+    return max(1, int(math.ceil(math.log2(max(per, 2.0)))))
 
 
 def motif_fine(name):
@@ -407,7 +419,8 @@ def main():
     with ClockSampler(local) as clk:
         for pi, (s_src, s_dst, s_t, n, rr) in enumerate(parts()):
             # C5 (coarse-only, hub-heavy): the pair index counts long closing windows (tm_graph_opts.pair_index)
-            g = T.Graph(s_src, s_dst, s_t, n, device=local, stream=stream, pair_index=CONFIG == "C5")
+            g = T.Graph(s_src, s_dst, s_t, n, device=local, stream=stream, pair_index=CONFIG == "C5",
+                        pair_id_bucket_log2=pair_bucket_log2(s_t))
             for _ in range(args.warmup):
                 step(g, rr)
             if lockstep:
@@ -446,7 +459,8 @@ def main():
                 hs, hd, ht = (x.numpy() for x in ph)
 
                 def e2e_step():
-                    gg = T.Graph(hs, hd, ht, n, device=local, stream=stream, pair_index=CONFIG == "C5")
+                    gg = T.Graph(hs, hd, ht, n, device=local, stream=stream, pair_index=CONFIG == "C5",
+                                 pair_id_bucket_log2=pair_bucket_log2(ht))
                     cs = ([T.tm_count(gg, mo, root_range=rr, stream=stream) for mo in motifs] if args.separate
                   else T.tm_count_multi(gg, motifs, root_range=rr, stream=stream))
                     gg.close()

@@ -70,6 +70,13 @@ typedef struct {
                              with two binary searches instead of a scan.  Pays off on
                              hub-heavy coarse-only queries (C5 slice: 232 -> 169 ms);
                              costs ~12 ms and 0.75 GB on a 63.5M-edge graph.  0: not built */
+    int pair_id_bucket_log2; /* with pair_index, k > 0: also a membership filter of
+                             (u, v, edge id >> k) — "the pair has an edge among these
+                             2^k consecutive edge ids".  A closing motif edge whose
+                             window (e_prev, H_δ(e_1)] covers at most 4 such buckets
+                             reads no list unless one of them may hold an edge of its
+                             pair.  Choose 2^k near the edge count of one δ.  8 bits
+                             per edge.  0: not built */
 } tm_graph_opts;
 
 /* Load a temporal graph G = {(src[i], dst[i], t[i])}, i < m and

@@ -144,6 +144,7 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
     base.m = (uint32_t)m;
     base.split = (uint32_t)(m + d.n);
     base.prec = d.prec; base.ptab = d.ptab; base.pmask = d.pmask; base.pbits = d.pbits; base.fmask = d.fmask;
+    base.tbits = d.tbits; base.tmask = d.tmask; base.tshift = d.tshift;
     if (roots_dev) {
         base.roots = roots_dev;
         base.n_roots = n_roots_list;

@@ -355,6 +355,16 @@ __global__ void k_pair_insert(const uint64_t *skey, uint64_t m, int nb, uint4 *t
     }
 }
 
+// id-bucketed pair filter: the bit of (src e, dst e, e >> shift) for every edge
+__global__ void k_pair_time_bits(const uint32_t *src, const uint32_t *dst, uint64_t m, int shift, uint32_t *bits,
+                                 uint32_t mask) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = ((uint64_t)src[e] << 32) | dst[e];
+        const uint32_t b = (uint32_t)(pair_bucket_hash(pair_hash(key), e >> shift) >> 32) & mask;
+        atomicOr(bits + (b >> 5), 1u << (b & 31));
+    }
+}
+
 __global__ void k_count_starts(const uint64_t *skey, uint64_t m, unsigned long long *cnt) {
     unsigned long long c = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
@@ -375,7 +385,7 @@ cudaError_t dmalloc(T **p, size_t count, cudaStream_t s) {
 
 void free_graph(DeviceGraph &d, cudaStream_t s) {
     for (void *q : {(void *)d.src, (void *)d.dst, (void *)d.t, (void *)d.perm, (void *)d.off_out, (void *)d.off_in,
-                    (void *)d.rec, (void *)d.rank, (void *)d.skip, (void *)d.prec, (void *)d.ptab, (void *)d.pbits,
+                    (void *)d.rec, (void *)d.rank, (void *)d.skip, (void *)d.prec, (void *)d.ptab, (void *)d.pbits, (void *)d.tbits,
                     (void *)d.vlab, (void *)d.elab})
         dev_free(q, s);
     if (d.nxc) {
@@ -445,7 +455,7 @@ done:
 
 // Pair index: stable radix sort of the edges by (src, dst), distinct pairs
 // counted, then inserted into the hash table.
-cudaError_t build_pairs(DeviceGraph &d, cudaStream_t s) {
+cudaError_t build_pairs(DeviceGraph &d, cudaStream_t s, int bucket_log2) {
     const uint64_t m = d.m;
     uint64_t *key = nullptr, *skey = nullptr;
     uint32_t *val = nullptr;
@@ -486,6 +496,15 @@ cudaError_t build_pairs(DeviceGraph &d, cudaStream_t s) {
         TRY(cudaMemsetAsync(d.pbits, 0, fb / 8, s));
     }
     if (m) k_pair_insert<<<grid_for(m), 256, 0, s>>>(skey, m, nb, d.ptab, d.pmask, d.pbits, d.fmask);
+    if (m && bucket_log2 > 0) {   // the id-bucketed filter: TM_BLOOM_BITS bits per edge
+        uint64_t tb = 1024;
+        while (tb < (uint64_t)TM_BLOOM_BITS * m) tb <<= 1;
+        d.tmask = (uint32_t)(tb - 1);
+        d.tshift = std::min(bucket_log2, 31);
+        TRY(dmalloc(&d.tbits, tb / 32, s));
+        TRY(cudaMemsetAsync(d.tbits, 0, tb / 8, s));
+        k_pair_time_bits<<<grid_for(m), 256, 0, s>>>(d.src, d.dst, m, d.tshift, d.tbits, d.tmask);
+    }
     TRY(cudaGetLastError());
     TRY(cudaStreamSynchronize(s));
 done:
@@ -881,7 +900,7 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
             TRY(cudaMemsetAsync(d.rec, 0xff, (2 * (m + n) + 32) * sizeof(uint64_t), s));
         } else {
             TRY(build_skip(d, s));
-            if (TM_PAIR_LEAF || TM_PAIR_NONLEAF || TM_PAIR_BUILD || (o && o->pair_index)) TRY(build_pairs(d, s));
+            if (TM_PAIR_LEAF || TM_PAIR_NONLEAF || TM_PAIR_BUILD || (o && o->pair_index)) TRY(build_pairs(d, s, o ? o->pair_id_bucket_log2 : 0));
             TRY(cudaStreamSynchronize(s));
             dev_free(flags, s);
             *out = g;
@@ -919,7 +938,7 @@ tm_status graph_create(const uint32_t *src, const uint32_t *dst, const int64_t *
     TRY(cudaGetLastError());
     TRY(build_csr(d, s));
     TRY(build_skip(d, s));
-    if (TM_PAIR_LEAF || TM_PAIR_NONLEAF || TM_PAIR_BUILD || (o && o->pair_index)) TRY(build_pairs(d, s));
+    if (TM_PAIR_LEAF || TM_PAIR_NONLEAF || TM_PAIR_BUILD || (o && o->pair_index)) TRY(build_pairs(d, s, o ? o->pair_id_bucket_log2 : 0));
     TRY(cudaStreamSynchronize(s));
 #undef TRY
     if (!on_dev) { dev_free(isrc, s); dev_free(idst, s); dev_free(it, s); }

@@ -681,7 +681,18 @@ struct Warp {
             if (plan.template u<NL>() < plan.template nv<NL>() && plan.template v<NL>() < plan.template nv<NL>() &&
                 p.ptab && live && !gen()) {
                 const uint64_t key = ((uint64_t)pick(phi, plan.template u<NL>()) << 32) | pick(phi, plan.template v<NL>());
-                live = pair_maybe(p.pbits, p.fmask, pair_hash(key));
+                const uint64_t ph = pair_hash(key);
+                const uint32_t b0 = (e + 1) >> p.tshift, b1 = hi >> p.tshift;   // the window lies in (e, hi]
+                if (p.tbits && b1 - b0 < 2u) {
+                    // id-bucketed filter: the pair must have an edge in one of the window's buckets
+                    const uint32_t bit0 = (uint32_t)(pair_bucket_hash(ph, b0) >> 32) & p.tmask;
+                    const uint32_t bit1 = (uint32_t)(pair_bucket_hash(ph, b1) >> 32) & p.tmask;
+                    const uint32_t w0 = __ldg(p.tbits + (bit0 >> 5)) >> (bit0 & 31);
+                    const uint32_t w1 = __ldg(p.tbits + (bit1 >> 5)) >> (bit1 & 31);
+                    live = (w0 | w1) & 1u;
+                } else {
+                    live = pair_maybe(p.pbits, p.fmask, ph);
+                }
             }
         }
 #ifdef TM_SKIP_LEAF   // timing experiment only (wrong counts): the cost of the closing level

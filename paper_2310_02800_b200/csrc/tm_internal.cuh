@@ -94,6 +94,11 @@ struct DeviceGraph {
     // an absent pair — the common case when closing a cycle — costs one L2 hit
     uint32_t *pbits = nullptr;
     uint32_t fmask = 0;
+    // id-bucketed pair filter (tm_graph_opts.pair_id_bucket_log2): one bit per
+    // hash of (u, v, id >> tshift); tbits == nullptr: not built
+    uint32_t *tbits = nullptr;
+    uint32_t tmask = 0;
+    int tshift = 0;
     // optional labels (tm_graph_set_labels): per vertex, per edge by sorted id
     int32_t *vlab = nullptr, *elab = nullptr;
     // lazily filled first-record ids (NextIdCache); owned, freed with the graph
@@ -128,6 +133,11 @@ __host__ __device__ inline uint64_t pair_hash(uint64_t k) {   // splitmix64 fina
     k *= 0x94d049bb133111ebull;
     k ^= k >> 31;
     return k;
+}
+
+// hash of a vertex pair in one edge-id bucket (the id-bucketed pair filter)
+__host__ __device__ inline uint64_t pair_bucket_hash(uint64_t pair_h, uint64_t bucket) {
+    return pair_hash(pair_h ^ (bucket * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull));
 }
 
 // filter bit positions of a pair hash; fmask = filter bits - 1
@@ -229,6 +239,9 @@ struct MineParams {
     uint32_t pmask;
     const uint32_t *pbits;
     uint32_t fmask;
+    const uint32_t *tbits;
+    uint32_t tmask;
+    int tshift;
     const uint32_t *H;                 // H_δ  (coarse δ-horizon)
     const uint32_t *Hf[kMaxL];         // H_{δ_i} per gap i, nullptr when δ_i = ∞
     const uint4 *HW[kMaxL];            // per gap i (TM_HRANK == 3): window descriptors {start, end, H_δi, 0}

@@ -35,7 +35,8 @@ class TMotifError(RuntimeError):
 
 
 class GraphOpts(ctypes.Structure):
-    _fields_ = [("device", _i32), ("stream", _P), ("input_on_device", _i32), ("pair_index", _i32)]
+    _fields_ = [("device", _i32), ("stream", _P), ("input_on_device", _i32), ("pair_index", _i32),
+                ("pair_id_bucket_log2", _i32)]
 
 
 class RunOpts(ctypes.Structure):
@@ -167,7 +168,8 @@ def run_opts(stream=None, root_range=None, edge_id_offset=0, canonical=False, bu
 class Graph:
     """tm_graph: device-resident sorted edge list + bidirectional CSR."""
 
-    def __init__(self, src, dst, t, n_vertices: int, *, device: int = -1, stream=None, pair_index: bool = False):
+    def __init__(self, src, dst, t, n_vertices: int, *, device: int = -1, stream=None, pair_index: bool = False,
+                 pair_id_bucket_log2: int = 0):
         L = lib()
         on_dev = _is_torch(src)
         if on_dev:
@@ -183,7 +185,7 @@ class Graph:
             t = np.ascontiguousarray(t, np.int64)
         self._keep = (src, dst, t)
         m = int(src.shape[0])
-        o = GraphOpts(device, _stream_handle(stream), int(on_dev), int(bool(pair_index)))
+        o = GraphOpts(device, _stream_handle(stream), int(on_dev), int(bool(pair_index)), int(pair_id_bucket_log2))
         h = _P()
         _check(L.tm_graph_create(_ptr(src), _ptr(dst), _ptr(t), m, int(n_vertices), ctypes.byref(o),
                                  ctypes.byref(h)))

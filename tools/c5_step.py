@@ -16,9 +16,10 @@ ap.add_argument("--parts", type=int, default=64)
 ap.add_argument("--part", type=int, default=3)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--no-pair", action="store_true", help="build the graph without the pair index")
+ap.add_argument("--bucket-log2", type=int, default=0, help="tm_graph_opts.pair_id_bucket_log2")
 a = ap.parse_args()
 s, d, t, n, nr = synth.c5_rank_slice(a.part, a.parts, 3600)
-g = T.Graph(s, d, t, n, pair_index=not a.no_pair)
+g = T.Graph(s, d, t, n, pair_index=not a.no_pair, pair_id_bucket_log2=a.bucket_log2)
 mos = [T.Motif(M.TRI, 3600), T.Motif(M.C4, 3600)]
 best = None
 for _ in range(a.reps):
