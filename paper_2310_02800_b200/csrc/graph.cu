@@ -359,8 +359,7 @@ __global__ void k_pair_insert(const uint64_t *skey, uint64_t m, int nb, uint4 *t
 __global__ void k_pair_time_bits(const uint32_t *src, const uint32_t *dst, uint64_t m, int shift, uint32_t *bits,
                                  uint32_t mask) {
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t key = ((uint64_t)src[e] << 32) | dst[e];
-        const uint32_t b = (uint32_t)(pair_bucket_hash(pair_hash(key), e >> shift) >> 32) & mask;
+        const uint32_t b = pair_bucket_bit(src[e], dst[e], (uint32_t)(e >> shift), mask);
         atomicOr(bits + (b >> 5), 1u << (b & 31));
     }
 }
@@ -497,8 +496,8 @@ cudaError_t build_pairs(DeviceGraph &d, cudaStream_t s, int bucket_log2) {
     }
     if (m) k_pair_insert<<<grid_for(m), 256, 0, s>>>(skey, m, nb, d.ptab, d.pmask, d.pbits, d.fmask);
     if (m && bucket_log2 > 0) {   // the id-bucketed filter: TM_BLOOM_BITS bits per edge
-        uint64_t tb = 1024;
-        while (tb < (uint64_t)TM_BLOOM_BITS * m) tb <<= 1;
+        uint64_t tb = 1024;   // bits, a power of two <= 2^32 (32-bit hash)
+        while (tb < (uint64_t)TM_BLOOM_BITS * m && tb < (1ull << 32)) tb <<= 1;
         d.tmask = (uint32_t)(tb - 1);
         d.tshift = std::min(bucket_log2, 31);
         TRY(dmalloc(&d.tbits, tb / 32, s));

@@ -680,17 +680,17 @@ struct Warp {
             // is an edge of this very vertex pair)
             if (plan.template u<NL>() < plan.template nv<NL>() && plan.template v<NL>() < plan.template nv<NL>() &&
                 p.ptab && live && !gen()) {
-                const uint64_t key = ((uint64_t)pick(phi, plan.template u<NL>()) << 32) | pick(phi, plan.template v<NL>());
-                const uint64_t ph = pair_hash(key);
+                const uint32_t pu = pick(phi, plan.template u<NL>()), pv = pick(phi, plan.template v<NL>());
                 const uint32_t b0 = (e + 1) >> p.tshift, b1 = hi >> p.tshift;   // the window lies in (e, hi]
                 if (p.tbits && b1 - b0 < 2u) {
                     // id-bucketed filter: the pair must have an edge in one of the window's buckets
-                    const uint32_t bit0 = (uint32_t)(pair_bucket_hash(ph, b0) >> 32) & p.tmask;
-                    const uint32_t bit1 = (uint32_t)(pair_bucket_hash(ph, b1) >> 32) & p.tmask;
+                    const uint32_t bit0 = pair_bucket_bit(pu, pv, b0, p.tmask);
+                    const uint32_t bit1 = pair_bucket_bit(pu, pv, b1, p.tmask);
                     const uint32_t w0 = __ldg(p.tbits + (bit0 >> 5)) >> (bit0 & 31);
                     const uint32_t w1 = __ldg(p.tbits + (bit1 >> 5)) >> (bit1 & 31);
                     live = (w0 | w1) & 1u;
                 } else {
+                    const uint64_t ph = pair_hash(((uint64_t)pu << 32) | pv);
                     live = pair_maybe(p.pbits, p.fmask, ph);
                 }
             }

@@ -135,9 +135,17 @@ __host__ __device__ inline uint64_t pair_hash(uint64_t k) {   // splitmix64 fina
     return k;
 }
 
-// hash of a vertex pair in one edge-id bucket (the id-bucketed pair filter)
-__host__ __device__ inline uint64_t pair_bucket_hash(uint64_t pair_h, uint64_t bucket) {
-    return pair_hash(pair_h ^ (bucket * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull));
+// bit of (pair u -> v, edge-id bucket b) in the id-bucketed pair filter: a
+// 32-bit multiply-add combination and the murmur3 finaliser (cheap: the
+// mining kernel evaluates it for every live closing leaf)
+__host__ __device__ inline uint32_t pair_bucket_bit(uint32_t u, uint32_t v, uint32_t b, uint32_t mask) {
+    uint32_t k = u * 0x9E3779B1u + v * 0x85EBCA77u + b * 0xC2B2AE3Du + 0x27D4EB2Fu;
+    k ^= k >> 16;
+    k *= 0x85EBCA6Bu;
+    k ^= k >> 13;
+    k *= 0xC2B2AE35u;
+    k ^= k >> 16;
+    return k & mask;
 }
 
 // filter bit positions of a pair hash; fmask = filter bits - 1
