@@ -102,6 +102,9 @@ def test_declared_struct_sizes_match_binding():
     assert T.KernelInfo.carried_by.offset == 24
     assert T.KernelInfo.kernel_mode.offset == 28
     assert ctypes.sizeof(T.SearchStats) == 8 * 13
+    # device, (pad), stream, input_on_device, pair_index, pair_id_bucket_log2, (pad)
+    assert ctypes.sizeof(T.GraphOpts) == 32
+    assert T.GraphOpts.stream.offset == 8 and T.GraphOpts.pair_id_bucket_log2.offset == 24
 
 
 def test_kernel_mode_constants_match_header():
