@@ -88,7 +88,10 @@ typedef struct {
  *   m        : 0 <= m <= TM_MAX_M; m == 0 is a valid empty graph
  *   o        : may be NULL (device -1, default stream, host input)
  * Ownership: the inputs are copied; the caller keeps them.  The library owns
- * *out and its device memory until tm_graph_destroy.  Self-loop edges are
+ * *out and its device memory until tm_graph_destroy (besides the CSR: the
+ * rank arrays, 16 B per edge, and the first-record-id cache, 32 B per edge,
+ * filled by the first query that needs each of its four list variants and
+ * reused by later ones — a property of the graph, independent of δ).  Self-loop edges are
  * kept (they take edge ids) but can never be matched (injectivity, Q4).
  * Errors: TM_EINVAL (null pointer with m > 0, id >= n_vertices, t < 0,
  * m > TM_MAX_M), TM_ENOMEM, TM_ECUDA. */
