@@ -438,6 +438,28 @@ tm_status run_multi(const tm_graph *g, const tm_motif *const *mos, uint32_t k, c
                 p.sib_rows = sib_region[b];
                 p.sib_cap = rows_needed[b] ? (uint32_t)sib_cap : 0u;
             }
+        // root pruning (TM_ROOT_PRUNE): every match of this motif closes with an edge
+        // in the root endpoint y's list inside (e_1, H_δ(e_1)] (the closing
+        // look-ahead window); when that window is empty the root has no
+        // match.  Only when no node count is needed (no prefix counting) and a
+        // sibling emitted by this kernel, if any, closes through the same list.
+        p.root_prune = 0;
+        if (TM_ROOT_PRUNE && (mode == kCount || mode == kEnum || mode == kRoots) && !mo->constrained() &&
+            !mo->disconnected && pmask[i] == 0) {
+            Shape sh{};
+            sh.L = (int)mo->L;
+            for (uint32_t j = 0; j < mo->L; j++) { sh.u[j] = mo->u[j]; sh.v[j] = mo->v[j]; }
+            bool ok = sh.look();
+            for (uint32_t b = 0; b < k && ok; b++)
+                if (sib_of[b] == (int)i) {
+                    const tm_motif *mb = mos[b];
+                    const uint32_t K = mb->L - 1;
+                    const int y = sh.lky();
+                    ok = sh.lkdir() == 1 ? ((int)mb->v[K] == y && (int)mb->u[K] != y)
+                                         : ((int)mb->u[K] == y && (int)mb->v[K] != y);
+                }
+            p.root_prune = ok ? 1u : 0u;
+        }
         const bool resuming = resume_of[i] >= 0;
         if (resuming) {   // continue from sibling b's rows
             const int b = resume_of[i];

@@ -77,6 +77,9 @@ constexpr int kLeafSectors = TM_LEAF_SECTORS;
 #ifndef TM_PAIR_FILTER
 #define TM_PAIR_FILTER 1    // 1: closing leaves test the pair index's membership filter first (graphs with one)
 #endif
+#ifndef TM_ROOT_PRUNE
+#define TM_ROOT_PRUNE 1     // roots with an empty closing look-ahead window are not searched (no prefix counts)
+#endif
 #ifndef TM_LEAF_TASK
 #define TM_LEAF_TASK 0      // 1: known leaf windows are pushed as tasks instead of scanned in the lane
 #endif
@@ -1057,8 +1060,10 @@ struct Warp {
             const uint32_t phi[2] = {a, bb};
             const uint32_t hi = ok ? ld_stream(p.H + r) : 0;   // t' = t_root + δ as an index
             uint32_t li = ~0u;
-            if constexpr (Layout<Plan, MODE>::look())
+            if constexpr (Layout<Plan, MODE>::look()) {
                 if (ok) li = look_ahead(r, hi);
+                if (TM_ROOT_PRUNE && li == 0u && p.root_prune) ok = false;   // no closing edge can exist
+            }
             push<1>(ok, r, hi, phi, eh, (uint32_t)slot, li);
         }
         return true;

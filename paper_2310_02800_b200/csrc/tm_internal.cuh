@@ -277,6 +277,7 @@ struct MineParams {
     // scratch[kPrefixBase + l]
     uint32_t prefix_mask;
     uint32_t prefix_lv0;               // lowest set level of prefix_mask (counted per lane)
+    uint32_t root_prune;               // 1: a root whose closing look-ahead window is empty is not searched
     // sibling emission (kCountPfx): at level sib_level, candidates whose
     // neighbour is φ[sib_vtx] complete a sibling motif's closing edge; their
     // rows (e_1..e_sib_level, e) go to sib_rows (cap rows), counted in
