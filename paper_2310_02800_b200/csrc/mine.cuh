@@ -80,6 +80,9 @@ constexpr int kLeafSectors = TM_LEAF_SECTORS;
 #ifndef TM_ROOT_PRUNE
 #define TM_ROOT_PRUNE 1     // roots with an empty closing look-ahead window are not searched (no prefix counts)
 #endif
+#ifndef TM_ROOT_CLAMP
+#define TM_ROOT_CLAMP 1     // with root pruning: the root's horizon clamps to its closing window's latest edge
+#endif
 #ifndef TM_LEAF_TASK
 #define TM_LEAF_TASK 0      // 1: known leaf windows are pushed as tasks instead of scanned in the lane
 #endif
@@ -983,7 +986,7 @@ struct Warp {
     // neighbours of y's list records in (r, hi]; 0 if there is none, all ones
     // if that window runs past the aligned sector holding its start (no
     // gallop: a superset is as correct, only less selective).
-    __device__ __forceinline__ uint32_t look_ahead(uint32_t r, uint32_t hi) const {
+    __device__ __forceinline__ uint32_t look_ahead(uint32_t r, uint32_t hi, uint32_t &last) const {
         const uint32_t b = ld_stream(p.rank + (size_t)Plan::lkvar() * p.m + r);   // first record after r
         const uint32_t a4 = b & ~3u;
         const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(p.rec + a4);
@@ -1003,8 +1006,12 @@ struct Warp {
 #pragma unroll
         for (int k = 0; k < NR; k++) {
             if (a4 + k < b || end) continue;
-            if ((uint32_t)(rr[k] >> 32) > hi) end = true;
-            else mask |= 1u << look_hash((uint32_t)rr[k]);
+            if ((uint32_t)(rr[k] >> 32) > hi) {
+                end = true;
+            } else {
+                mask |= 1u << look_hash((uint32_t)rr[k]);
+                last = (uint32_t)(rr[k] >> 32);   // the window's latest edge so far
+            }
         }
         return end ? mask : ~0u;
     }
@@ -1058,11 +1065,17 @@ struct Warp {
             emit(ok, eh, r, (uint32_t)slot);
         } else if constexpr (LM > 1) {
             const uint32_t phi[2] = {a, bb};
-            const uint32_t hi = ok ? ld_stream(p.H + r) : 0;   // t' = t_root + δ as an index
+            uint32_t hi = ok ? ld_stream(p.H + r) : 0;   // t' = t_root + δ as an index
             uint32_t li = ~0u;
             if constexpr (Layout<Plan, MODE>::look()) {
-                if (ok) li = look_ahead(r, hi);
-                if (TM_ROOT_PRUNE && li == 0u && p.root_prune) ok = false;   // no closing edge can exist
+                uint32_t last = hi;
+                if (ok) li = look_ahead(r, hi, last);
+                if (TM_ROOT_PRUNE && p.root_prune) {
+                    if (li == 0u) ok = false;   // no closing edge can exist
+                    // the closing edge is the match's last and latest edge, and it lies
+                    // in this window: no edge of a match comes after the window's latest
+                    else if (TM_ROOT_CLAMP && li != ~0u) hi = last;
+                }
             }
             push<1>(ok, r, hi, phi, eh, (uint32_t)slot, li);
         }
