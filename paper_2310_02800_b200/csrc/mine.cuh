@@ -80,6 +80,9 @@ constexpr int kLeafSectors = TM_LEAF_SECTORS;
 #ifndef TM_ROOT_PRUNE
 #define TM_ROOT_PRUNE 1     // roots with an empty closing look-ahead window are not searched (no prefix counts)
 #endif
+#ifndef TM_LOOK_EXTRA
+#define TM_LOOK_EXTRA 7     // with root pruning: sectors of the look-ahead window read past the first
+#endif
 #ifndef TM_ROOT_CLAMP
 #define TM_ROOT_CLAMP 1     // with root pruning: the root's horizon clamps to its closing window's latest edge
 #endif
@@ -256,6 +259,30 @@ static_assert(kLookRecs == 4 || kLookRecs == 8 || kLookRecs == 12, "kLookRecs");
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t *q) {
     if (TM_STREAM_HINT) return __ldcs(q);
     return __ldg(q);
+}
+
+// bit of vertex v in a closing look-ahead mask (Fibonacci hashing)
+__device__ __forceinline__ uint32_t look_hash(uint32_t v);
+
+// The rest of a closing look-ahead window past its first sector (root
+// pruning): from position a (sector-aligned), up to TM_LOOK_EXTRA sectors.
+// Returns {mask, latest id} with the records <= hi folded into mask / last,
+// or {~0u, last} if the window runs on past them.
+static __device__ __noinline__ uint2 look_more(const uint64_t *__restrict__ rec, uint32_t a, uint32_t hi, uint32_t mask,
+                                        uint32_t last) {
+    const ulonglong2 *vp = reinterpret_cast<const ulonglong2 *>(rec + a);
+#pragma unroll 1
+    for (int q = 0; q < TM_LOOK_EXTRA; q++) {
+        const ulonglong2 x0 = __ldg(vp + 2 * q), x1 = __ldg(vp + 2 * q + 1);
+        const uint64_t r4[4] = {x0.x, x0.y, x1.x, x1.y};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if ((uint32_t)(r4[k] >> 32) > hi) return make_uint2(mask, last);
+            mask |= 1u << look_hash((uint32_t)r4[k]);
+            last = (uint32_t)(r4[k] >> 32);
+        }
+    }
+    return make_uint2(~0u, last);
 }
 
 // bit of vertex v in a closing look-ahead mask (Fibonacci hashing)
@@ -1012,6 +1039,13 @@ struct Warp {
                 mask |= 1u << look_hash((uint32_t)rr[k]);
                 last = (uint32_t)(rr[k] >> 32);   // the window's latest edge so far
             }
+        }
+        if (TM_LOOK_EXTRA && !end && p.root_prune) {
+            // pruning roots: follow the window up to TM_LOOK_EXTRA more sectors (the
+            // clamp and the prune need its end; the mask only gets less selective);
+            // out of line, so kernels that never prune keep their register allocation
+            const uint2 ml = look_more(p.rec, a4 + 4, hi, mask, last);
+            if (ml.x != ~0u) { mask = ml.x; last = ml.y; end = true; }
         }
         return end ? mask : ~0u;
     }
