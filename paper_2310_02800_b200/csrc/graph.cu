@@ -605,7 +605,7 @@ constexpr bool kNx4 = TM_NEXT_IDS == 4;
 // windows on C4) is written without reading any record.  nxw: record them
 // (the id of the record at the window start, from the sector read anyway).
 #ifndef TM_HR_MINB
-#define TM_HR_MINB 1
+#define TM_HR_MINB 5   // 5 resident 256-thread blocks per SM (48 registers, no spills): passes -0.07 ms; 6: +0.28 ms
 #endif
 __global__ void __launch_bounds__(256, TM_HR_MINB) k_hrank(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ skip,
                                                const uint32_t *__restrict__ rank, const uint32_t *__restrict__ H,
